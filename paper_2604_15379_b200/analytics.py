@@ -1,0 +1,106 @@
+"""Closed-form locality / roofline models and the decode-step byte budget.
+
+The first three functions restate the reference's pure formulas
+(``/root/reference/pkg/src/chipletsim/analytics.py:27-49``) and are used as
+the *predicted* column next to measured L2 hit rates.  :func:`fit_tiles`
+follows ``scenario.py:83-106``.  :func:`decode_step_bytes` is the algorithmic
+HBM byte count of one decode step that ``bench.py`` divides by the measured
+step time.
+"""
+
+from __future__ import annotations
+
+from .machine import MachineConfig, ModelConfig
+from .taskgraph import LINEAR_OPS, STANDARD_TILE_PROFILE, OpKind
+
+
+class AnalyticsError(ValueError):
+    pass
+
+
+def weight_hit_model(workers: int, batch: int, t_m: int) -> float:
+    """(R-1)/R with R = min(W, ceil(B/T_M)) (ref analytics.py:27-33)."""
+    if min(workers, batch, t_m) < 1:
+        raise AnalyticsError("workers, batch, and t_m must be positive")
+    r = min(workers, -(-batch // t_m))
+    return 1.0 - 1.0 / r
+
+
+def effective_ai(batch: int, l2_hit_rate: float) -> float:
+    """B / (1 - h) (ref analytics.py:36-42)."""
+    if batch < 1:
+        raise AnalyticsError("batch must be positive")
+    if not (0.0 <= l2_hit_rate < 1.0):
+        raise AnalyticsError("l2_hit_rate must lie in [0, 1)")
+    return batch / (1.0 - l2_hit_rate)
+
+
+def roofline(ai: float, machine: MachineConfig) -> float:
+    """min(peak, bw * ai) (ref analytics.py:45-49)."""
+    if ai < 0:
+        raise AnalyticsError("arithmetic intensity must be nonnegative")
+    return min(machine.peak_flops, machine.hbm_bandwidth_bytes_per_s * ai)
+
+
+def linear_gemm_dims(op: OpKind, model: ModelConfig) -> tuple:
+    """(K, N) of a linear op (ref analytics.py:71-83)."""
+    table = {
+        OpKind.QKV_PROJ: (model.hidden_dim, model.qkv_dim),
+        OpKind.O_PROJ_RESIDUAL: (model.hidden_dim, model.hidden_dim),
+        OpKind.GATE_UP_SILU: (model.hidden_dim, model.gate_up_dim),
+        OpKind.DOWN_PROJ_RESIDUAL: (model.ffn_dim, model.hidden_dim),
+    }
+    if op not in table:
+        raise AnalyticsError(f"{op.value} is not a linear op")
+    return table[op]
+
+
+def fit_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
+              base: dict | None = None) -> dict:
+    """Halve T_N / T_K until they divide the model's GEMMs (ref scenario.py:83-106).
+
+    ``base`` optionally replaces the starting tiles (the reference starts
+    from the standard profile or 16x64x256).
+    """
+    out = {}
+    for op in LINEAR_OPS:
+        k, n = linear_gemm_dims(op, model)
+        width = n if graph_mode == "standard" else n // machine.num_xcds
+        if op is OpKind.GATE_UP_SILU and graph_mode == "chiplet":
+            width //= 2
+        if base is not None:
+            t_m, t_n, t_k = base[op]
+        elif graph_mode == "standard":
+            t_m, t_n, t_k = STANDARD_TILE_PROFILE[op]
+        else:
+            t_m, t_n, t_k = (16, 64, 256)
+        while width % t_n:
+            t_n //= 2
+        while k % t_k:
+            t_k //= 2
+        out[op] = (t_m, t_n, t_k)
+    out["silu_chunk"] = min(STANDARD_TILE_PROFILE["silu_chunk"], model.ffn_dim)
+    return out
+
+
+def layer_weight_bytes(model: ModelConfig) -> int:
+    d, f = model.hidden_dim, model.ffn_dim
+    lin = d * model.qkv_dim + d * d + d * model.gate_up_dim + f * d
+    norms = 2 * d + 2 * model.head_dim  # rms1/rms2 gammas + q_norm/k_norm
+    return (lin + norms) * model.dtype_bytes
+
+
+def decode_step_bytes(model: ModelConfig, batch: int, ctx: int,
+                      vocab: int, layers: int | None = None) -> dict:
+    """Algorithmic HBM bytes of one decode step.
+
+    weights (every layer + final norm + LM head) + KV read of ``ctx`` cached
+    tokens per sequence.  Activations are ignored (they are <0.1% and stay
+    in L2).
+    """
+    L = model.num_layers if layers is None else layers
+    dt = model.dtype_bytes
+    w = L * layer_weight_bytes(model) + model.hidden_dim * dt \
+        + vocab * model.hidden_dim * dt
+    kv = batch * ctx * L * 2 * model.kv_heads * model.head_dim * dt
+    return {"weights": w, "kv": kv, "total": w + kv}
