@@ -83,6 +83,35 @@ def fit_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
     return out
 
 
+def device_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
+                 t_m: int = 16, t_n: int = 8, max_t_k: int = 1024) -> dict:
+    """B200 tile overrides for the CUDA-core GEMM body.
+
+    One shared-memory ring slot holds ``R x T_K`` bf16 with ``R = T_N`` (or
+    ``2*T_N`` for the fused gate/up die task) and ``R*T_K <= 8192`` (16 KiB);
+    ``T_K`` is the largest power of two <= ``max_t_k`` dividing K, ``T_N``
+    the largest power of two <= ``t_n`` dividing the per-task width.  Passing
+    the result as ``tile_overrides`` to both builders keeps graph parity.
+    """
+    out = {}
+    for op in LINEAR_OPS:
+        k, n = linear_gemm_dims(op, model)
+        fused = op is OpKind.GATE_UP_SILU and graph_mode == "chiplet"
+        width = n if graph_mode == "standard" else n // machine.num_xcds
+        if fused:
+            width //= 2
+        tk = max_t_k
+        while k % tk:
+            tk //= 2
+        rows_cap = min(32 // (2 if fused else 1), 8192 // tk // (2 if fused else 1))
+        tn = min(t_n, rows_cap)
+        while width % tn:
+            tn //= 2
+        out[op] = (t_m, max(tn, 1), tk)
+    out["silu_chunk"] = min(STANDARD_TILE_PROFILE["silu_chunk"], model.ffn_dim)
+    return out
+
+
 def layer_weight_bytes(model: ModelConfig) -> int:
     d, f = model.hidden_dim, model.ffn_dim
     lin = d * model.qkv_dim + d * d + d * model.gate_up_dim + f * d

@@ -1,0 +1,1509 @@
+// mk_kernel.cu -- the persistent hierarchical-task megakernel (sm_100a).
+//
+// One cooperative launch = one decode step.  grid = #SMs, one CTA per SM
+// (dynamic shared memory forces it).  Each CTA reads %smid, looks up its die
+// in the probed table and takes a role:
+//
+//   rank 0 of a die  -> scheduler CTA of that die (PER_DIE) -- or rank 0 of
+//                       the GPU in FLAT mode (die-unaware baseline)
+//   rank 1..W        -> worker w = rank-1 of that scheduler
+//
+// Scheduler (one warp): walks its die's dispatch list (topological order,
+// host-lowered from the TaskGraph) and writes worker mailboxes: a die task
+// (reference CHIPLET level) is broadcast to all W workers of its die, a CU
+// task unit goes to the next worker round-robin (ref runtime.py:301-307,
+// 373-417).  It does not wait for dependencies: dispatch runs ahead so the
+// workers can stream weights early; dependencies are resolved by the worker
+// with gpu-scope acquire loads on the event counters.
+//
+// Worker: warp 0 is the fetch warp -- it reads the mailbox, forwards units to
+// the consumer warps through a shared-memory queue, and streams every weight
+// tile (and every cached K/V block) the unit will need into a 12-slot shared
+// memory ring with TMA bulk copies (L2 evict_first), ignoring dependencies
+// (weights and past KV are immutable during the step).  Warps 1..8 are the
+// consumers: wait on the unit's events, run the op body, signal completion
+// with two-level counting (ref runtime.py:432-480):
+//   die task : atom.acq_rel on the die-local counter; the W-th arrival on
+//              the die issues fence.acq_rel.gpu + red.release.gpu on the
+//              event counter (one fence + one global atomic per die per event)
+//   CU task  : red.release.gpu on the event counter (fanned-out CU tasks count
+//              their units on a sub-counter first).
+//
+// Counters are monotone across launches: the event fires in step e (epoch,
+// 1-based) when counter >= required * e, so no per-step reset is needed.
+#include <cuda_runtime.h>
+#include <cooperative_groups.h>
+#include <cstdio>
+#include <cstring>
+#include <cmath>
+#include <vector>
+#include <string>
+#include <algorithm>
+
+#include "mk.h"
+#include "mk_ptx.cuh"
+
+namespace mk {
+
+constexpr int kConsWarps = 8;
+constexpr int kCons = kConsWarps * 32;          // consumer threads
+constexpr int kThreads = kCons + 32;            // + fetch warp
+constexpr int kSlotBytes = 16384;
+constexpr int kSlots = 12;
+constexpr int kTQ = 32;                         // smem unit queue depth
+constexpr int kMailbox = 64;                    // mailbox depth per worker
+constexpr uint32_t kEnd = 0xFFFFFFu;
+constexpr int kMaxNB = 16;
+constexpr int kAmaxRows = 64;
+
+enum StatIdx {
+  S_DISPATCH = 0, S_MAILBOX, S_GLOBAL, S_LOCAL, S_FENCE, S_FANOUT, S_POLL,
+  S_TILES, S_EXEC, S_STEPS, S_N
+};
+
+struct KArgs {
+  const mk_task* tasks;
+  const mk_unit* units;
+  const int32_t* sched_begin;
+  const uint8_t* params;
+  uint32_t* ev_ctr;
+  const int32_t* ev_req;
+  uint32_t* die_ctr;       // [n_events][n_sched]
+  uint32_t* sub_ctr;
+  uint64_t* mailbox;       // [n_sched*W][kMailbox]
+  uint64_t* mb_head;       // consumer progress per worker (persistent)
+  uint64_t* mb_tail;       // scheduler progress per worker (persistent)
+  const int8_t* die_of_sm;
+  uint32_t* role_ctr;      // [n_groups]
+  const int32_t* group_size;
+  unsigned long long* stats;
+  mk_log_rec* log;
+  unsigned long long* log_cursor;
+  long long log_cap;
+  int32_t* tile_log;
+  unsigned long long* tile_cursor;
+  long long tile_cap;
+  int* err;
+  int* err_info;
+  unsigned long long watchdog_ns;
+  int n_events;
+  int n_sched;
+  int sched_mode;
+  int W;
+  uint32_t epoch;
+};
+
+struct Smem {
+  uint64_t full[kSlots];
+  uint64_t empty[kSlots];
+  uint64_t tq_full[kTQ];
+  uint64_t tq_empty[kTQ];
+  int4 tq[kTQ];
+  float red[4][32][kMaxNB];         // GEMM cross-warp partial sums
+  float am_val[kAmaxRows];          // LM-head running max per row
+  int am_idx[kAmaxRows];
+  float vec[8][128];                // attention: rotated q per head
+  float kn[128], vn[128];           // attention: new token k / v
+  float st[8][288];                 // attention: per-(warp,token-group) state;
+                                    // also the prologue's pre-rope scratch
+  float bred[32];
+  int ibred[32];
+  int4 cur;                         // consumer broadcast: current unit
+  int abort_flag;
+};
+
+// Scheduler CTAs never use the ring: their mailbox cursors live there.
+struct SchedSmem {
+  uint64_t tail[MK_MAX_SMS];
+  uint64_t head[MK_MAX_SMS];
+};
+
+constexpr size_t kRingOffset = (sizeof(Smem) + 1023) / 1024 * 1024;
+constexpr size_t kSmemBytes = kRingOffset + size_t(kSlots) * kSlotBytes;
+
+__device__ __forceinline__ bool aborted(const KArgs& a) {
+  return *reinterpret_cast<volatile int*>(a.err) != 0;
+}
+
+__device__ __noinline__ void raise_deadlock(const KArgs& a, int info) {
+  if (atomicCAS(a.err, 0, MK_ERR_DEADLOCK) == 0) *a.err_info = info;
+}
+
+// Spin helper: returns false if the watchdog fired / the launch aborted.
+struct Spin {
+  uint64_t t0 = 0;
+  uint32_t n = 0;
+  __device__ __forceinline__ bool ok(const KArgs& a, int info) {
+    if ((++n & 255u) == 0) {
+      if (aborted(a)) return false;
+      uint64_t now = globaltimer();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > a.watchdog_ns) { raise_deadlock(a, info); return false; }
+    }
+    return true;
+  }
+};
+
+__device__ __forceinline__ bool mbar_wait(const KArgs& a, uint64_t* bar, uint32_t parity, int info) {
+  Spin sp;
+  while (!mbar_try_wait(bar, parity)) {
+    if (!sp.ok(a, info)) return false;
+  }
+  return true;
+}
+
+template <typename T>
+__device__ __forceinline__ const T* P(const KArgs& a, const mk_task& t) {
+  return reinterpret_cast<const T*>(a.params + t.param_off);
+}
+
+// ---------------------------------------------------------------------------
+// Tile iteration shared by the fetch warp and the consumers (ref
+// traversal.py:125-202 restated as an owner-inverse loop).
+// ---------------------------------------------------------------------------
+struct TileIter {
+  int mt, nt, W, w, trav, dist, xcd;
+  int idx, row, n, fixed_m, fixed_n, done;
+  __device__ void init(const mk_gemm_params& p, int workers, int worker) {
+    const int rows_per_out = (p.epilogue == MK_EPI_SILU) ? 2 : 1;
+    mt = (p.M + p.T_M - 1) / p.T_M;
+    nt = p.N / (p.T_N * rows_per_out);
+    W = workers; w = worker; trav = p.traversal; dist = p.distribution;
+    xcd = p.xcd; fixed_m = p.tile_m; fixed_n = p.tile_n; done = 0;
+    idx = w; row = 0; n = w;
+  }
+  __device__ bool next(int& m_out, int& n_out) {
+    if (fixed_m >= 0) {              // standard-mode CU tile task
+      if (done) return false;
+      done = 1; m_out = fixed_m; n_out = fixed_n; return true;
+    }
+    if (dist == MK_DIST_M_SPLIT) {
+      while (row < mt) {
+        if (n < nt) {
+          m_out = (xcd % mt + row) % mt; n_out = n; n += W; return true;
+        }
+        ++row; n = w;
+      }
+      return false;
+    }
+    if (idx >= mt * nt) return false;
+    if (trav == MK_TRAV_M_MAJOR) { m_out = idx % mt; n_out = idx / mt; }
+    else { m_out = idx / nt; n_out = idx % nt; }
+    idx += W;
+    return true;
+  }
+};
+
+__device__ __forceinline__ int gemm_rows(const mk_gemm_params& p) {
+  return p.T_N * (p.epilogue == MK_EPI_SILU ? 2 : 1);
+}
+
+// ---------------------------------------------------------------------------
+// Fetch warp: stream the unit's immutable operands into the ring.
+// ---------------------------------------------------------------------------
+struct Ring {
+  uint32_t k = 0;   // slots issued / consumed so far this launch
+};
+
+__device__ bool fetch_slot(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
+                           const void* src, uint32_t bytes, uint64_t pol) {
+  const int i = r.k % kSlots;
+  const uint32_t round = r.k / kSlots;
+  if (!mbar_wait(a, &s.empty[i], (round & 1) ^ 1, -2)) return false;
+  mbar_arrive_expect_tx(&s.full[i], bytes);
+  bulk_g2s(ring + size_t(i) * kSlotBytes, src, bytes, &s.full[i], pol);
+  ++r.k;
+  return true;
+}
+
+__device__ bool fetch_unit(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
+                           const mk_task& t, int ib, int ie, int worker, uint64_t pol) {
+  if (t.op == MK_OP_GEMM) {
+    const mk_gemm_params& p = *P<mk_gemm_params>(a, t);
+    const int R = gemm_rows(p);
+    const int chunks = p.K / p.T_K;
+    const uint32_t bytes = uint32_t(R) * p.T_K * 2;
+    TileIter it;
+    it.init(p, a.W, t.level == MK_LEVEL_CHIPLET ? worker : 0);
+    int m, n;
+    const __nv_bfloat16* w = reinterpret_cast<const __nv_bfloat16*>(p.w);
+    while (it.next(m, n)) {
+      const __nv_bfloat16* tile = w + size_t(n) * chunks * R * p.T_K;
+      for (int c = 0; c < chunks; ++c)
+        if (!fetch_slot(a, s, ring, r, tile + size_t(c) * R * p.T_K, bytes, pol)) return false;
+    }
+  } else if (t.op == MK_OP_ATTN_PARTIAL) {
+    const mk_attn_params& p = *P<mk_attn_params>(a, t);
+    for (int i = ib; i < ie; ++i) {
+      const int b = i / p.n_splits, sp = i % p.n_splits;
+      const int pos = p.positions[b];
+      const int t0 = sp * p.split;
+      if (t0 > pos) continue;
+      const int nc = min(p.split, pos - t0);
+      if (nc <= 0) continue;
+      const size_t row = (size_t(b) * p.kv_heads + p.kv_head) * p.t_max + t0;
+      const uint32_t bytes = uint32_t(nc) * p.head_dim * 2;
+      const __nv_bfloat16* kc = reinterpret_cast<const __nv_bfloat16*>(p.k_cache);
+      const __nv_bfloat16* vc = reinterpret_cast<const __nv_bfloat16*>(p.v_cache);
+      if (!fetch_slot(a, s, ring, r, kc + row * p.head_dim, bytes, pol)) return false;
+      if (!fetch_slot(a, s, ring, r, vc + row * p.head_dim, bytes, pol)) return false;
+    }
+  }
+  return true;
+}
+
+// Consumer-side slot handshake.  After an abort the wait just stops (the
+// data is garbage, the launch result is discarded) so that every consumer
+// thread keeps the same control flow and no named barrier can hang.
+__device__ __forceinline__ void cons_wait_slot(const KArgs& a, Smem& s, const Ring& r) {
+  const int i = r.k % kSlots;
+  mbar_wait(a, &s.full[i], (r.k / kSlots) & 1, -3);
+}
+__device__ __forceinline__ void cons_release_slot(Smem& s, Ring& r) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(&s.empty[r.k % kSlots]);
+  ++r.k;
+}
+
+// ---------------------------------------------------------------------------
+// GEMM tile body: y[m0:m0+rows, cols] = x[m0:.., :] . W_tile^T  (CUDA cores,
+// 128-bit weight streaming; weights come from the smem ring).
+// Slot layout: [R rows][T_K] bf16, thread ct owns 16-byte segments
+// ct, ct+256, ... -- all in one column (x reuse across rows).
+// ---------------------------------------------------------------------------
+template <int NB>
+__device__ void gemm_tile(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
+                          const mk_gemm_params& p, int m, int n, int ct,
+                          int worker_slot) {
+  const int R = gemm_rows(p);
+  const int KC = p.T_K;
+  const int spr = KC / 8;                 // segments per row (divides 256)
+  const int segs = R * spr;               // <= 1024
+  const int col8 = ct % spr;
+  const int rbase = ct / spr;
+  const int rstep = kCons / spr;
+  const int chunks = p.K / KC;
+  const int m0 = m * p.T_M;
+  const int rows_m = min(p.T_M, p.M - m0);
+  const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(p.x);
+
+  float acc[4][NB];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[j][b] = 0.f;
+
+  for (int c = 0; c < chunks; ++c) {
+    cons_wait_slot(a, s, r);
+    const uint8_t* slot = ring + size_t(r.k % kSlots) * kSlotBytes;
+    const int kbase = c * KC + col8 * 8;
+    if constexpr (NB <= 8) {
+      float xf[NB][8];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        if (b < rows_m) {
+          uint4 v = ldg128_cg(x + size_t(m0 + b) * p.ldx + kbase);
+          unpack8(v, xf[b]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) xf[b][e] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int sg = ct + j * kCons;
+        if (sg < segs) {
+          float wf[8];
+          unpack8(lds128(slot + size_t(sg) * 16), wf);
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            float t = acc[j][b];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) t = fmaf(wf[e], xf[b][e], t);
+            acc[j][b] = t;
+          }
+        }
+      }
+    } else {
+      uint4 xr[NB];
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        xr[b] = (b < rows_m) ? ldg128_cg(x + size_t(m0 + b) * p.ldx + kbase) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int sg = ct + j * kCons;
+        if (sg < segs) {
+          float wf[8];
+          unpack8(lds128(slot + size_t(sg) * 16), wf);
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            float xf[8];
+            unpack8(xr[b], xf);
+            float t = acc[j][b];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) t = fmaf(wf[e], xf[e], t);
+            acc[j][b] = t;
+          }
+        }
+      }
+    }
+    cons_release_slot(s, r);
+  }
+
+  // reduce the spr threads of each row: shuffles inside the warp, then smem
+  const int lanes = spr < 32 ? spr : 32;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      float v = acc[j][b];
+      for (int off = lanes >> 1; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      acc[j][b] = v;
+    }
+  const int wsub = col8 / 32;
+  if ((col8 % lanes) == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int sg = ct + j * kCons;
+      if (sg < segs) {
+        const int row = rbase + j * rstep;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) s.red[wsub][row][b] = acc[j][b];
+      }
+    }
+  }
+  bar_sync(1, kCons);
+  const int nsub = (spr + 31) / 32;
+  const int out_rows = p.T_N;
+  const int out_col0 = p.y_col0 + n * p.T_N;
+  auto rowsum = [&](int row, int b) {
+    float v = 0.f;
+    for (int q = 0; q < nsub; ++q) v += s.red[q][row][b];
+    return v;
+  };
+  if (p.epilogue == MK_EPI_LOGITS) {
+    float* y = reinterpret_cast<float*>(p.y);
+    for (int e = ct; e < out_rows * rows_m; e += kCons) {
+      const int rr = e / rows_m, b = e % rows_m;
+      const float v = rowsum(rr, b);
+      if (y) y[size_t(m0 + b) * p.ldy + out_col0 + rr] = v;
+    }
+    if (ct < rows_m) {
+      const int b = m0 + ct;
+      float best = s.am_val[b];
+      int bi = s.am_idx[b];
+      for (int rr = 0; rr < out_rows; ++rr) {
+        const float v = rowsum(rr, ct);
+        const int col = out_col0 + rr;
+        if (v > best || (v == best && col < bi)) { best = v; bi = col; }
+      }
+      s.am_val[b] = best;
+      s.am_idx[b] = bi;
+    }
+  } else {
+    uint16_t* y = reinterpret_cast<uint16_t*>(p.y);
+    const uint16_t* res = reinterpret_cast<const uint16_t*>(p.res);
+    for (int e = ct; e < out_rows * rows_m; e += kCons) {
+      const int rr = e / rows_m, b = e % rows_m;
+      float v = rowsum(rr, b);
+      const size_t col = size_t(out_col0 + rr);
+      if (p.epilogue == MK_EPI_SILU) {
+        const float u = rowsum(rr + p.T_N, b);
+        v = v / (1.f + __expf(-v)) * u;
+      } else if (p.epilogue == MK_EPI_RESIDUAL) {
+        v += bf2f(ldg16_cg(res + size_t(m0 + b) * p.ldres + col));
+      }
+      y[size_t(m0 + b) * p.ldy + col] = f2bf(v);
+    }
+  }
+  bar_sync(1, kCons);   // red[] reused by the next tile
+  (void)worker_slot;
+}
+
+__device__ void run_gemm(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
+                         const mk_task& t, int worker, int gw, int tix, int ct,
+                         unsigned long long& tiles) {
+  const mk_gemm_params& p = *P<mk_gemm_params>(a, t);
+  const bool logits = p.epilogue == MK_EPI_LOGITS;
+  const int w_in_task = t.level == MK_LEVEL_CHIPLET ? worker : 0;
+  if (logits) {
+    for (int b = ct; b < p.M && b < kAmaxRows; b += kCons) {
+      s.am_val[b] = -INFINITY;
+      s.am_idx[b] = 0x7fffffff;
+    }
+    bar_sync(1, kCons);
+  }
+  TileIter it;
+  it.init(p, a.W, w_in_task);
+  int m, n;
+  while (it.next(m, n)) {
+    const int rows_m = min(p.T_M, p.M - m * p.T_M);
+    if (rows_m <= 1) gemm_tile<1>(a, s, ring, r, p, m, n, ct, w_in_task);
+    else if (rows_m <= 2) gemm_tile<2>(a, s, ring, r, p, m, n, ct, w_in_task);
+    else if (rows_m <= 4) gemm_tile<4>(a, s, ring, r, p, m, n, ct, w_in_task);
+    else if (rows_m <= 8) gemm_tile<8>(a, s, ring, r, p, m, n, ct, w_in_task);
+    else gemm_tile<16>(a, s, ring, r, p, m, n, ct, w_in_task);
+    if (ct == 0) {
+      ++tiles;
+      if (a.tile_log) {
+        unsigned long long at = atomicAdd(a.tile_cursor, 1ull);
+        if ((long long)at < a.tile_cap) {
+          int32_t* rec = a.tile_log + at * 4;
+          rec[0] = tix; rec[1] = gw; rec[2] = m; rec[3] = n;
+        }
+      }
+    }
+  }
+  if (logits) {
+    const int slot = p.amax_base + w_in_task;
+    for (int b = ct; b < p.M && b < kAmaxRows; b += kCons) {
+      p.amax_val[size_t(slot) * p.amax_stride + b] = s.am_val[b];
+      p.amax_idx[size_t(slot) * p.amax_stride + b] = s.am_idx[b];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// RMSNorm (Qwen3RMSNorm: fp32 statistics, cast, gamma multiply), optional
+// embedding gather for layer 0.
+// ---------------------------------------------------------------------------
+__device__ float block_sum(Smem& s, float v, int ct) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  if ((ct & 31) == 0) s.bred[ct >> 5] = v;
+  bar_sync(1, kCons);
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < kConsWarps; ++w) tot += s.bred[w];
+  bar_sync(1, kCons);
+  return tot;
+}
+
+__device__ void run_rmsnorm(const KArgs& a, Smem& s, const mk_task& t, int ib, int ie, int ct) {
+  const mk_norm_params& p = *P<mk_norm_params>(a, t);
+  const uint16_t* gam = reinterpret_cast<const uint16_t*>(p.gamma);
+  for (int b = ib; b < ie; ++b) {
+    const uint16_t* src;
+    if (p.embed) src = reinterpret_cast<const uint16_t*>(p.embed) + size_t(p.tokens[b]) * p.d;
+    else src = reinterpret_cast<const uint16_t*>(p.x) + size_t(b) * p.d;
+    float ss = 0.f;
+    for (int k = ct * 8; k < p.d; k += kCons * 8) {
+      float f[8];
+      unpack8(ldg128_cg(src + k), f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ss = fmaf(f[e], f[e], ss);
+    }
+    const float tot = block_sum(s, ss, ct);
+    const float rs = rsqrtf(tot / float(p.d) + p.eps);
+    uint16_t* y = reinterpret_cast<uint16_t*>(p.y) + size_t(b) * p.d;
+    uint16_t* xs = p.x_store ? reinterpret_cast<uint16_t*>(p.x_store) + size_t(b) * p.d : nullptr;
+    for (int k = ct * 8; k < p.d; k += kCons * 8) {
+      const uint4 raw = ldg128_cg(src + k);
+      float f[8], g[8];
+      unpack8(raw, f);
+      unpack8(ldg128_cg(gam + k), g);
+      uint16_t o[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float xn = bf2f(f2bf(f[e] * rs));   // hidden_states.to(input_dtype)
+        o[e] = f2bf(g[e] * xn);                   // weight * hidden_states
+      }
+      *reinterpret_cast<uint4*>(y + k) = *reinterpret_cast<uint4*>(o);
+      if (xs) *reinterpret_cast<uint4*>(xs + k) = raw;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Attention partial: QK-norm + RoPE (+ KV append for the new token) and a
+// split-KV online-softmax partial over cached tokens streamed into the ring.
+// ---------------------------------------------------------------------------
+template <int HD>
+__device__ void head_norm_rope(Smem& s, const uint16_t* src, const uint16_t* gam, float eps,
+                               const float* cs, const float* sn, float* out, int lane,
+                               float* scratch) {
+  float v[(HD + 31) / 32];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < (HD + 31) / 32; ++k) {
+    const int d = lane + 32 * k;
+    v[k] = d < HD ? bf2f(ldg16_cg(src + d)) : 0.f;
+    ss = fmaf(v[k], v[k], ss);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+  const float rs = rsqrtf(ss / float(HD) + eps);
+#pragma unroll
+  for (int k = 0; k < (HD + 31) / 32; ++k) {
+    const int d = lane + 32 * k;
+    if (d < HD) scratch[d] = bf2f(gam[d]) * bf2f(f2bf(v[k] * rs));
+  }
+  __syncwarp();
+  constexpr int H2 = HD / 2;
+  for (int i = lane; i < H2; i += 32) {
+    const float x1 = scratch[i], x2 = scratch[i + H2];
+    const float c = cs[i], sv = sn[i];
+    out[i] = x1 * c - x2 * sv;
+    out[i + H2] = x2 * c + x1 * sv;
+  }
+  __syncwarp();
+  (void)s;
+}
+
+template <int HD>
+__device__ void attn_item(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
+                          const mk_attn_params& p, int item, int ct) {
+  const int b = item / p.n_splits, sp = item % p.n_splits;
+  const int pos = p.positions[b];
+  const int t0 = sp * p.split;
+  if (t0 > pos) return;
+  const int nc = min(p.split, pos - t0);
+  const bool has_new = pos < t0 + p.split;
+  const int G = p.group;
+  const int warp = ct >> 5, lane = ct & 31;
+  const uint16_t* qkv = reinterpret_cast<const uint16_t*>(p.qkv) + size_t(b) * p.ldqkv;
+  const float* cs = p.rope_cos + size_t(pos) * (HD / 2);
+  const float* sn = p.rope_sin + size_t(pos) * (HD / 2);
+
+  // prologue: q heads of this group (warps 0..G-1), new k (warp G%8 after)
+  if (warp < G) {
+    const int qh = p.kv_head * G + warp;
+    head_norm_rope<HD>(s, qkv + qh * HD, reinterpret_cast<const uint16_t*>(p.q_gamma), p.eps,
+                       cs, sn, s.vec[warp], lane, s.st[warp]);
+  }
+  if (has_new) {
+    const int kw = G < kConsWarps ? G : 0;
+    if (G == kConsWarps) bar_sync(1, kCons);
+    if (warp == kw) {
+      const int koff = p.q_heads * HD + p.kv_head * HD;
+      const int voff = (p.q_heads + p.kv_heads) * HD + p.kv_head * HD;
+      head_norm_rope<HD>(s, qkv + koff, reinterpret_cast<const uint16_t*>(p.k_gamma), p.eps,
+                         cs, sn, s.kn, lane, s.st[kw]);
+      const size_t crow = ((size_t(b) * p.kv_heads + p.kv_head) * p.t_max + pos) * HD;
+      uint16_t* kc = reinterpret_cast<uint16_t*>(p.k_cache) + crow;
+      uint16_t* vc = reinterpret_cast<uint16_t*>(p.v_cache) + crow;
+      for (int d = lane; d < HD; d += 32) {
+        const uint16_t vv = ldg16_cg(qkv + voff + d);
+        const uint16_t kb = f2bf(s.kn[d]);
+        s.vn[d] = bf2f(vv);
+        kc[d] = kb;
+        vc[d] = vv;
+        s.kn[d] = bf2f(kb);      // attend to the rounded (cached) key, as later steps will
+      }
+    }
+  }
+  bar_sync(1, kCons);
+
+  constexpr int LPT = HD / 8;          // lanes per token
+  constexpr int TPI = 32 / LPT;        // tokens per warp iteration
+  const int head = warp % G, sub = warp / G, nsub = kConsWarps / G;
+  const int tg = lane / LPT, dl = lane % LPT;
+  const float qscale = p.scale * 1.4426950408889634f;
+  float q8[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) q8[e] = s.vec[head][dl * 8 + e] * qscale;
+
+  const uint8_t* kslot = nullptr;
+  const uint8_t* vslot = nullptr;
+  if (nc > 0) {
+    cons_wait_slot(a, s, r);
+    kslot = ring + size_t(r.k % kSlots) * kSlotBytes;
+    Ring r2 = r; ++r2.k;
+    cons_wait_slot(a, s, r2);
+    vslot = ring + size_t(r2.k % kSlots) * kSlotBytes;
+  }
+  float mx = -INFINITY, l = 0.f, o[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) o[e] = 0.f;
+  const int ntot = nc + (has_new ? 1 : 0);
+  for (int tb = sub * TPI; tb < ntot; tb += nsub * TPI) {
+    const int tk = tb + tg;
+    const bool valid = tk < ntot;
+    float kf[8], vf[8];
+    if (valid && tk < nc) {
+      unpack8(lds128(kslot + size_t(tk) * HD * 2 + dl * 16), kf);
+      unpack8(lds128(vslot + size_t(tk) * HD * 2 + dl * 16), vf);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        kf[e] = valid ? s.kn[dl * 8 + e] : 0.f;
+        vf[e] = valid ? s.vn[dl * 8 + e] : 0.f;
+      }
+    }
+    float sc = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sc = fmaf(q8[e], kf[e], sc);
+#pragma unroll
+    for (int off = LPT >> 1; off > 0; off >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, off);
+    if (valid) {
+      const float mn = fmaxf(mx, sc);
+      const float corr = exp2f(mx - mn);
+      const float pr = exp2f(sc - mn);
+      l = l * corr + pr;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = fmaf(o[e], corr, pr * vf[e]);
+      mx = mn;
+    }
+  }
+  if (nc > 0) {
+    cons_release_slot(s, r);
+    cons_release_slot(s, r);
+  }
+  // combine the (warp, token-group) states of each head
+  bar_sync(1, kCons);            // prologue scratch (s.st) no longer read
+  float* st = s.st[warp] + tg * (HD + 2);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) st[dl * 8 + e] = o[e];
+  if (dl == 0) { st[HD] = mx; st[HD + 1] = l; }
+  bar_sync(1, kCons);
+  float* part = p.partial + ((size_t(b) * p.kv_heads + p.kv_head) * p.n_splits + sp) * G * (HD + 4);
+  for (int e = ct; e < G * HD; e += kCons) {
+    const int hh = e / HD, d = e % HD;
+    float M = -INFINITY;
+    for (int q = 0; q < nsub; ++q)
+      for (int g2 = 0; g2 < TPI; ++g2) M = fmaxf(M, s.st[q * G + hh][g2 * (HD + 2) + HD]);
+    float acc = 0.f, den = 0.f;
+    for (int q = 0; q < nsub; ++q)
+      for (int g2 = 0; g2 < TPI; ++g2) {
+        const float* x = s.st[q * G + hh] + g2 * (HD + 2);
+        if (x[HD] == -INFINITY) continue;
+        const float f = exp2f(x[HD] - M);
+        acc = fmaf(f, x[d], acc);
+        den = fmaf(f, x[HD + 1], den);
+      }
+    float* dst = part + size_t(hh) * (HD + 4);
+    dst[d] = acc;
+    if (d == 0) { dst[HD] = M; dst[HD + 1] = den; }
+  }
+  bar_sync(1, kCons);
+}
+
+__device__ void run_attn_partial(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
+                                 const mk_task& t, int ib, int ie, int ct) {
+  const mk_attn_params& p = *P<mk_attn_params>(a, t);
+  for (int i = ib; i < ie; ++i) {
+    switch (p.head_dim) {
+      case 128: attn_item<128>(a, s, ring, r, p, i, ct); break;
+      case 64: attn_item<64>(a, s, ring, r, p, i, ct); break;
+      case 32: attn_item<32>(a, s, ring, r, p, i, ct); break;
+      default: attn_item<16>(a, s, ring, r, p, i, ct); break;
+    }
+  }
+}
+
+__device__ void run_attn_reduce(const KArgs& a, const mk_task& t, int ib, int ie, int ct) {
+  const mk_attn_params& p = *P<mk_attn_params>(a, t);
+  const int HD = p.head_dim, G = p.group;
+  uint16_t* out = reinterpret_cast<uint16_t*>(p.out);
+  for (int b = ib; b < ie; ++b) {
+    const int pos = p.positions[b];
+    const int nv = pos / p.split + 1;
+    const float* base = p.partial + (size_t(b) * p.kv_heads + p.kv_head) * p.n_splits * G * (HD + 4);
+    for (int e = ct; e < G * HD; e += kCons) {
+      const int hh = e / HD, d = e % HD;
+      float M = -INFINITY;
+      for (int sp = 0; sp < nv; ++sp)
+        M = fmaxf(M, __ldcg(base + (size_t(sp) * G + hh) * (HD + 4) + HD));
+      float num = 0.f, den = 0.f;
+      for (int sp = 0; sp < nv; ++sp) {
+        const float* x = base + (size_t(sp) * G + hh) * (HD + 4);
+        const float f = exp2f(__ldcg(x + HD) - M);
+        num = fmaf(f, __ldcg(x + d), num);
+        den = fmaf(f, __ldcg(x + HD + 1), den);
+      }
+      out[size_t(b) * p.q_heads * HD + (p.kv_head * G + hh) * HD + d] = f2bf(num / den);
+    }
+  }
+}
+
+__device__ void run_silu(const KArgs& a, const mk_task& t, int ct) {
+  const mk_silu_params& p = *P<mk_silu_params>(a, t);
+  const uint16_t* gu = reinterpret_cast<const uint16_t*>(p.gu);
+  uint16_t* y = reinterpret_cast<uint16_t*>(p.y);
+  for (int e = ct; e < p.rows * p.cols; e += kCons) {
+    const int rr = p.row0 + e / p.cols, c = p.col0 + e % p.cols;
+    const float g = bf2f(ldg16_cg(gu + size_t(rr) * 2 * p.F + c));
+    const float u = bf2f(ldg16_cg(gu + size_t(rr) * 2 * p.F + p.F + c));
+    y[size_t(rr) * p.F + c] = f2bf(g / (1.f + __expf(-g)) * u);
+  }
+}
+
+__device__ void run_argmax(const KArgs& a, Smem& s, const mk_task& t, int ib, int ie, int ct) {
+  const mk_argmax_params& p = *P<mk_argmax_params>(a, t);
+  for (int b = ib; b < ie; ++b) {
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int q = ct; q < p.n_slots; q += kCons) {
+      const float v = __ldcg(p.amax_val + size_t(q) * p.M + b);
+      const int i = __ldcg(p.amax_idx + size_t(q) * p.M + b);
+      if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float v2 = __shfl_xor_sync(0xffffffffu, best, off);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (v2 > best || (v2 == best && i2 < bi)) { best = v2; bi = i2; }
+    }
+    if ((ct & 31) == 0) { s.bred[ct >> 5] = best; s.ibred[ct >> 5] = bi; }
+    bar_sync(1, kCons);
+    if (ct == 0) {
+      for (int w = 1; w < kConsWarps; ++w) {
+        const float v2 = s.bred[w];
+        const int i2 = s.ibred[w];
+        if (v2 > best || (v2 == best && i2 < bi)) { best = v2; bi = i2; }
+      }
+      p.out_tokens[b] = bi;
+      p.next_tokens[b] = bi;
+      p.positions[b] = p.positions[b] + 1;
+    }
+    bar_sync(1, kCons);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Roles
+// ---------------------------------------------------------------------------
+__device__ void log_rec(const KArgs& a, int kind, int task, int ib, int worker, int die,
+                        uint64_t t0, uint64_t t1) {
+  unsigned long long at = atomicAdd(a.log_cursor, 1ull);
+  if ((long long)at >= a.log_cap) return;
+  mk_log_rec& r = a.log[at];
+  r.kind = kind; r.task = task; r.item_begin = ib; r.worker = worker;
+  r.smid = (int)smid(); r.die = die; r.t_start = t0; r.t_end = t1;
+}
+
+__device__ void scheduler(const KArgs& a, SchedSmem& s, int g) {
+  const int lane = threadIdx.x & 31;
+  const int W = a.W;
+  const int gw0 = g * W;
+  for (int w = lane; w < W; w += 32) {
+    s.tail[w] = a.mb_tail[gw0 + w];
+    s.head[w] = ld_acquire64(&a.mb_head[gw0 + w]);
+  }
+  __syncwarp();
+  unsigned long long n_disp = 0, n_mail = 0;
+  bool alive = true;
+  auto push = [&](int w, uint32_t payload) -> bool {
+    uint64_t t = s.tail[w];
+    Spin sp;
+    while (t - s.head[w] >= (uint64_t)kMailbox) {
+      s.head[w] = ld_acquire64(&a.mb_head[gw0 + w]);
+      if (!sp.ok(a, -4)) return false;
+    }
+    st_release64(&a.mailbox[size_t(gw0 + w) * kMailbox + t % kMailbox],
+                 ((t + 1) << 24) | payload);
+    s.tail[w] = t + 1;
+    return true;
+  };
+  const int begin = a.sched_begin[g], end = a.sched_begin[g + 1];
+  int rr = 0;
+  int i = begin;
+  const int batch = W < 32 ? W : 32;
+  while (i < end && alive) {
+    const mk_unit u = a.units[i];
+    const mk_task& t = a.tasks[u.task];
+    if (t.level == MK_LEVEL_CHIPLET) {
+      uint64_t t0 = a.log ? globaltimer() : 0;
+      for (int w = lane; w < W && alive; w += 32) alive = push(w, (uint32_t)i);
+      alive = __all_sync(0xffffffffu, alive);
+      if (lane == 0) {
+        ++n_disp; n_mail += W;
+        if (a.log) log_rec(a, 0, u.task, u.item_begin, -1 - g, g, t0, globaltimer());
+      }
+      ++i;
+    } else {
+      // a run of consecutive CU units, one per lane, distinct workers
+      const int j = i + lane;
+      bool cu = false;
+      if (lane < batch && j < end) cu = a.tasks[a.units[j].task].level != MK_LEVEL_CHIPLET;
+      const unsigned msk = __ballot_sync(0xffffffffu, !cu);
+      const int run = msk ? (__ffs(msk) - 1) : 32;
+      if (lane < run) {
+        uint64_t t0 = a.log ? globaltimer() : 0;
+        alive = push((rr + lane) % W, (uint32_t)j);
+        if (a.log) log_rec(a, 0, a.units[j].task, a.units[j].item_begin, -1 - g, g, t0, globaltimer());
+      }
+      alive = __all_sync(0xffffffffu, alive);
+      if (lane == 0) { n_disp += run; n_mail += run; }
+      rr = (rr + run) % W;
+      i += run;
+    }
+  }
+  for (int w = lane; w < W && alive; w += 32) alive = push(w, kEnd);
+  __syncwarp();
+  for (int w = lane; w < W; w += 32) a.mb_tail[gw0 + w] = s.tail[w];
+  if (lane == 0) {
+    atomicAdd(&a.stats[S_DISPATCH], n_disp);
+    atomicAdd(&a.stats[S_MAILBOX], n_mail);
+  }
+}
+
+__device__ void fetch_warp(const KArgs& a, Smem& s, uint8_t* ring, int g, int worker) {
+  if ((threadIdx.x & 31) != 0) return;
+  const int gw = g * a.W + worker;
+  uint64_t head = a.mb_head[gw];
+  const uint64_t pol = policy_evict_first();
+  Ring r;
+  uint32_t q = 0;
+  for (;;) {
+    uint64_t e;
+    Spin sp;
+    const uint64_t* slotp = &a.mailbox[size_t(gw) * kMailbox + head % kMailbox];
+    for (;;) {
+      e = ld_acquire64(slotp);
+      if ((e >> 24) == head + 1) break;
+      if (!sp.ok(a, -5)) { e = kEnd; break; }
+    }
+    const uint32_t payload = uint32_t(e & 0xFFFFFFu);
+    if ((e >> 24) == head + 1) {
+      ++head;
+      st_release64(&a.mb_head[gw], head);
+    }
+    const int qi = q % kTQ;
+    if (!mbar_wait(a, &s.tq_empty[qi], ((q / kTQ) & 1) ^ 1, -6)) {
+      s.tq[qi] = make_int4(-1, 0, 0, 0);
+      mbar_arrive(&s.tq_full[qi]);
+      return;
+    }
+    if (payload == kEnd) {
+      s.tq[qi] = make_int4(-1, 0, 0, 0);
+      mbar_arrive(&s.tq_full[qi]);
+      return;
+    }
+    const mk_unit u = a.units[payload];
+    s.tq[qi] = make_int4(u.task, u.item_begin, u.item_end, 0);
+    mbar_arrive(&s.tq_full[qi]);
+    ++q;
+    if (!fetch_unit(a, s, ring, r, a.tasks[u.task], u.item_begin, u.item_end, worker, pol)) {
+      // aborted: make sure the consumers see an end marker eventually
+      return;
+    }
+  }
+}
+
+__device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int worker) {
+  const int ct = threadIdx.x - 32;
+  const int gw = g * a.W + worker;
+  Ring r;
+  uint32_t q = 0;
+  unsigned long long n_glob = 0, n_loc = 0, n_fence = 0, n_fan = 0, n_poll = 0, n_tiles = 0,
+                     n_exec = 0;
+  uint64_t t_start = 0;
+  for (;;) {
+    const int qi = q % kTQ;
+    // thread 0 takes the next unit and resolves its dependencies; the
+    // decision is broadcast through shared memory so that all consumer
+    // threads follow the same control flow (no divergent named barriers)
+    if (ct == 0) {
+      int4 ent = make_int4(-1, 0, 0, 0);
+      if (mbar_wait(a, &s.tq_full[qi], (q / kTQ) & 1, -7)) ent = s.tq[qi];
+      if (ent.x >= 0) {
+        const mk_task& t = a.tasks[ent.x];
+        const int waits[2] = {t.wait0, t.wait1};
+        for (int k = 0; k < 2; ++k) {
+          const int e = waits[k];
+          if (e < 0) continue;
+          const uint32_t target = uint32_t(a.ev_req[e]) * a.epoch;
+          Spin sp;
+          for (;;) {
+            ++n_poll;
+            if ((int32_t)(ld_acquire(&a.ev_ctr[e]) - target) >= 0) break;
+            if (!sp.ok(a, e)) break;
+          }
+        }
+        if (a.log) t_start = globaltimer();
+      }
+      s.cur = ent;
+      s.abort_flag = aborted(a) ? 1 : 0;
+    }
+    bar_sync(1, kCons);
+    const int4 ent = s.cur;
+    if (ent.x < 0 || s.abort_flag) break;
+    const mk_task& t = a.tasks[ent.x];
+    switch (t.op) {
+      case MK_OP_GEMM: run_gemm(a, s, ring, r, t, worker, gw, ent.x, ct, n_tiles); break;
+      case MK_OP_RMSNORM: run_rmsnorm(a, s, t, ent.y, ent.z, ct); break;
+      case MK_OP_ATTN_PARTIAL: run_attn_partial(a, s, ring, r, t, ent.y, ent.z, ct); break;
+      case MK_OP_ATTN_REDUCE: run_attn_reduce(a, t, ent.y, ent.z, ct); break;
+      case MK_OP_SILU: run_silu(a, t, ct); break;
+      case MK_OP_ARGMAX: run_argmax(a, s, t, ent.y, ent.z, ct); break;
+      default: break;
+    }
+    bar_sync(1, kCons);
+    if (ct == 0) {
+      ++n_exec;
+      if (t.signal >= 0) {
+        if (t.level == MK_LEVEL_CHIPLET) {
+          const uint32_t old = atom_acq_rel_add(&a.die_ctr[size_t(t.signal) * a.n_sched + g], 1u);
+          ++n_loc;
+          if (old + 1 == uint32_t(a.W) * a.epoch) {
+            fence_acq_rel_gpu();
+            ++n_fence;
+            red_release_add(&a.ev_ctr[t.signal], 1u);
+            ++n_glob;
+          }
+        } else if (t.n_units > 1) {
+          const uint32_t old = atom_acq_rel_add(&a.sub_ctr[t.sub_ctr], 1u);
+          ++n_fan;
+          if (old + 1 == uint32_t(t.n_units) * a.epoch) {
+            red_release_add(&a.ev_ctr[t.signal], 1u);
+            ++n_glob;
+          }
+        } else {
+          red_release_add(&a.ev_ctr[t.signal], 1u);
+          ++n_glob;
+        }
+      }
+      if (a.log) log_rec(a, 1, ent.x, ent.y, gw, g, t_start, globaltimer());
+      mbar_arrive(&s.tq_empty[qi]);
+    }
+    ++q;
+  }
+  if (ct == 0) {
+    atomicAdd(&a.stats[S_GLOBAL], n_glob);
+    atomicAdd(&a.stats[S_LOCAL], n_loc);
+    atomicAdd(&a.stats[S_FENCE], n_fence);
+    atomicAdd(&a.stats[S_FANOUT], n_fan);
+    atomicAdd(&a.stats[S_POLL], n_poll);
+    atomicAdd(&a.stats[S_TILES], n_tiles);
+    atomicAdd(&a.stats[S_EXEC], n_exec);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) megakernel(const KArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem& s = *reinterpret_cast<Smem*>(smem_raw);
+  uint8_t* ring = smem_raw + kRingOffset;
+  __shared__ int role[2];
+  if (threadIdx.x == 0) {
+    const int die = a.die_of_sm[smid()];
+    const int g = a.sched_mode == MK_SCHED_FLAT ? 0 : die;
+    const uint32_t raw = atomicAdd(&a.role_ctr[g], 1u);
+    const int rank = int(raw - (a.epoch - 1) * uint32_t(a.group_size[g]));
+    role[0] = g;
+    role[1] = rank;
+    for (int i = 0; i < kSlots; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], kConsWarps); }
+    for (int i = 0; i < kTQ; ++i) { mbar_init(&s.tq_full[i], 1); mbar_init(&s.tq_empty[i], 1); }
+    fence_mbar_init();
+    if (blockIdx.x == 0) atomicAdd(&a.stats[S_STEPS], 1ull);
+  }
+  __syncthreads();
+  const int g = role[0], rank = role[1];
+  if (g >= a.n_sched) return;
+  if (rank == 0) {
+    if (threadIdx.x < 32) scheduler(a, *reinterpret_cast<SchedSmem*>(ring), g);
+    return;
+  }
+  const int worker = rank - 1;
+  if (worker >= a.W) return;             // extra SMs of the larger die idle
+  if (threadIdx.x < 32) fetch_warp(a, s, ring, g, worker);
+  else consumers(a, s, ring, g, worker);
+}
+
+// ---------------------------------------------------------------------------
+// Die probe: per-SM L2 hit latency to lines spread over the address space.
+// ---------------------------------------------------------------------------
+__global__ void probe_init(uint32_t* buf, int n_lines, int stride_words) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_lines; i += gridDim.x * blockDim.x)
+    buf[size_t(i) * stride_words] = uint32_t(i) * uint32_t(stride_words);   // self-pointer
+}
+
+// Each CTA (one per SM) times a dependent chain of .cg loads (L2 hits) on
+// every probe line; the clock is read behind a branch on the last loaded
+// value so it cannot issue before the chain completes.
+__global__ void __launch_bounds__(32, 1) probe_kernel(const uint32_t* buf, int n_lines, int stride_words,
+                                                      int reps, uint32_t* lat, int* smid_of_block) {
+  extern __shared__ uint8_t pad_smem[];
+  if (threadIdx.x != 0) return;
+  pad_smem[0] = 0;
+  const uint32_t sm = smid();
+  smid_of_block[blockIdx.x] = int(sm);
+  constexpr int kChain = 16;
+  for (int i = 0; i < n_lines; ++i) {
+    uint32_t best = 0xffffffffu;
+    uint32_t idx = uint32_t(i) * uint32_t(stride_words);
+    for (int rep = 0; rep < reps; ++rep) {
+      const long long t0 = clock64();
+#pragma unroll
+      for (int c = 0; c < kChain; ++c)
+        asm volatile("ld.global.cg.u32 %0, [%1];" : "=r"(idx) : "l"(buf + idx) : "memory");
+      if (idx == 0xffffffffu) smid_of_block[0] = -2;   // forces the chain to finish
+      const long long t1 = clock64();
+      if (rep > 0) best = min(best, uint32_t((t1 - t0) / kChain));
+    }
+    lat[size_t(sm) * n_lines + i] = best;
+  }
+}
+
+}  // namespace mk
+
+// ===========================================================================
+// Host side: C ABI
+// ===========================================================================
+using namespace mk;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(MK_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct mk_handle {
+  int device = 0;
+  int num_sms = 0;
+  int sched_mode = 0;
+  int n_sched = 0;
+  int W = 0;
+  int n_events = 0, n_tasks = 0, n_units = 0, n_sub = 0;
+  uint32_t epoch = 0;
+  double watchdog_s = 5.0;
+  // device buffers
+  mk_task* d_tasks = nullptr;
+  mk_unit* d_units = nullptr;
+  int32_t* d_sched_begin = nullptr;
+  uint8_t* d_params = nullptr;
+  uint32_t* d_ev_ctr = nullptr;
+  int32_t* d_ev_req = nullptr;
+  uint32_t* d_die_ctr = nullptr;
+  uint32_t* d_sub_ctr = nullptr;
+  uint64_t* d_mailbox = nullptr;
+  uint64_t* d_mb_head = nullptr;
+  uint64_t* d_mb_tail = nullptr;
+  int8_t* d_die_of_sm = nullptr;
+  uint32_t* d_role_ctr = nullptr;
+  int32_t* d_group_size = nullptr;
+  unsigned long long* d_stats = nullptr;
+  int* d_err = nullptr;
+  int* h_err = nullptr;   // pinned copy
+  mk_log_rec* d_log = nullptr;
+  unsigned long long* d_log_cursor = nullptr;
+  long long log_cap = 0;
+  int32_t* d_tile_log = nullptr;
+  unsigned long long* d_tile_cursor = nullptr;
+  long long tile_cap = 0;
+  std::vector<int32_t> group_size;
+};
+
+template <typename T>
+static int dalloc(T** p, size_t n) {
+  CK(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T)));
+  return MK_OK;
+}
+
+extern "C" {
+
+const char* mk_last_error(void) { return g_err.c_str(); }
+int mk_version(void) { return 1; }
+
+static int probe_raw(int device, std::vector<uint32_t>& h, std::vector<int>& sm_of, int& nsm,
+                     int& n_lines) {
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  nsm = prop.multiProcessorCount;
+  if (nsm > MK_MAX_SMS) return fail(MK_ERR_CONFIG, "too many SMs");
+  n_lines = 512;
+  const int stride_words = 1024 + 32, reps = 8;   // 4 KiB + 128 B apart
+  uint32_t* buf = nullptr;
+  uint32_t* lat = nullptr;
+  int* smid_of_block = nullptr;
+  CK(cudaMalloc(&buf, size_t(n_lines) * stride_words * 4));
+  CK(cudaMemset(buf, 0, size_t(n_lines) * stride_words * 4));
+  probe_init<<<4, 128>>>(buf, n_lines, stride_words);
+  CK(cudaGetLastError());
+  CK(cudaMalloc(&lat, size_t(MK_MAX_SMS) * n_lines * 4));
+  CK(cudaMemset(lat, 0, size_t(MK_MAX_SMS) * n_lines * 4));
+  CK(cudaMalloc(&smid_of_block, nsm * sizeof(int)));
+  const int pad = 160 * 1024;   // one block per SM
+  CK(cudaFuncSetAttribute(probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pad));
+  probe_kernel<<<nsm, 32, pad>>>(buf, n_lines, stride_words, reps, lat, smid_of_block);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  h.assign(size_t(MK_MAX_SMS) * n_lines, 0);
+  sm_of.assign(nsm, 0);
+  CK(cudaMemcpy(h.data(), lat, h.size() * 4, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(sm_of.data(), smid_of_block, nsm * sizeof(int), cudaMemcpyDeviceToHost));
+  cudaFree(buf); cudaFree(lat); cudaFree(smid_of_block);
+  return MK_OK;
+}
+
+int mk_probe_raw(int device, uint32_t* lat_out, int32_t* n_lines_out) {
+  std::vector<uint32_t> h;
+  std::vector<int> sm_of;
+  int nsm = 0, n_lines = 0;
+  int rc = probe_raw(device, h, sm_of, nsm, n_lines);
+  if (rc) return rc;
+  if (lat_out) memcpy(lat_out, h.data(), h.size() * 4);
+  if (n_lines_out) *n_lines_out = n_lines;
+  return MK_OK;
+}
+
+int mk_probe(int device, mk_topology* out) {
+  if (!out) return fail(MK_ERR_CONFIG, "null topology");
+  std::vector<uint32_t> h;
+  std::vector<int> sm_of;
+  int nsm = 0, n_lines = 0;
+  int rc = probe_raw(device, h, sm_of, nsm, n_lines);
+  if (rc) return rc;
+  // which smids exist
+  std::vector<int> present(MK_MAX_SMS, 0);
+  int max_sm = 0;
+  for (int b = 0; b < nsm; ++b) { present[sm_of[b]] = 1; max_sm = std::max(max_sm, sm_of[b]); }
+  std::vector<int> sms;
+  for (int i = 0; i <= max_sm; ++i) if (present[i]) sms.push_back(i);
+  // bit pattern: latency above the line's median across SMs
+  std::vector<double> med(n_lines);
+  for (int i = 0; i < n_lines; ++i) {
+    std::vector<uint32_t> col;
+    for (int sm : sms) col.push_back(h[size_t(sm) * n_lines + i]);
+    std::nth_element(col.begin(), col.begin() + col.size() / 2, col.end());
+    med[i] = col[col.size() / 2];
+  }
+  auto bits = [&](int sm, int i) { return double(h[size_t(sm) * n_lines + i]) > med[i] ? 1 : 0; };
+  // 2-means on the bit vectors, seeded with the first SM
+  std::vector<int> label(MK_MAX_SMS, -1);
+  const int ref = sms[0];
+  for (int sm : sms) {
+    int d = 0;
+    for (int i = 0; i < n_lines; ++i) d += bits(sm, i) != bits(ref, i);
+    label[sm] = d * 2 > n_lines ? 1 : 0;
+  }
+  for (int iter = 0; iter < 4; ++iter) {
+    std::vector<double> cen(2 * n_lines, 0.0);
+    int cnt[2] = {0, 0};
+    for (int sm : sms) {
+      ++cnt[label[sm]];
+      for (int i = 0; i < n_lines; ++i) cen[label[sm] * n_lines + i] += h[size_t(sm) * n_lines + i];
+    }
+    if (cnt[0] == 0 || cnt[1] == 0) break;
+    for (int c = 0; c < 2; ++c)
+      for (int i = 0; i < n_lines; ++i) cen[c * n_lines + i] /= cnt[c];
+    for (int sm : sms) {
+      double d0 = 0, d1 = 0;
+      for (int i = 0; i < n_lines; ++i) {
+        const double v = h[size_t(sm) * n_lines + i];
+        d0 += (v - cen[i]) * (v - cen[i]);
+        d1 += (v - cen[n_lines + i]) * (v - cen[n_lines + i]);
+      }
+      label[sm] = d1 < d0 ? 1 : 0;
+    }
+  }
+  int cnt[2] = {0, 0};
+  for (int sm : sms) ++cnt[label[sm]];
+  // near/far latencies: a line's home die is the cluster that sees it faster
+  double near_sum = 0, far_sum = 0;
+  long near_n = 0, far_n = 0;
+  double var = 0;
+  if (cnt[0] > 0 && cnt[1] > 0) {
+    for (int i = 0; i < n_lines; ++i) {
+      double m[2] = {0, 0};
+      for (int sm : sms) m[label[sm]] += h[size_t(sm) * n_lines + i];
+      m[0] /= cnt[0]; m[1] /= cnt[1];
+      const int home = m[0] <= m[1] ? 0 : 1;
+      for (int sm : sms) {
+        const double v = h[size_t(sm) * n_lines + i];
+        if (label[sm] == home) { near_sum += v; ++near_n; } else { far_sum += v; ++far_n; }
+        var += (v - m[label[sm]]) * (v - m[label[sm]]);
+      }
+    }
+  }
+  memset(out, 0, sizeof(*out));
+  out->num_sms = nsm;
+  for (int i = 0; i < MK_MAX_SMS; ++i) out->die_of_sm[i] = 0;
+  const bool split_ok = cnt[0] > 0 && cnt[1] > 0 && near_n > 0 && far_n > 0;
+  if (split_ok) {
+    out->near_cycles = float(near_sum / near_n);
+    out->far_cycles = float(far_sum / far_n);
+    const double sd = std::sqrt(var / double(near_n + far_n)) + 1e-9;
+    out->separation = float((out->far_cycles - out->near_cycles) / sd);
+    out->num_dies = 2;
+    // die 0 holds the lowest smid
+    const int flip = label[sms[0]];
+    for (int sm : sms) out->die_of_sm[sm] = label[sm] ^ flip;
+    out->sms_per_die[0] = cnt[flip];
+    out->sms_per_die[1] = cnt[flip ^ 1];
+  } else {
+    out->num_dies = 1;
+    out->sms_per_die[0] = nsm;
+    out->separation = 0.f;
+  }
+  return MK_OK;
+}
+
+static int validate_graph(const mk_graph_desc* g) {
+  if (!g || !g->tasks || !g->event_required || !g->units || !g->sched_begin)
+    return fail(MK_ERR_CONFIG, "null graph arrays");
+  if (g->n_schedulers < 1 || g->workers_per_sched < 1)
+    return fail(MK_ERR_CONFIG, "bad scheduler / worker count");
+  if (g->sched_begin[0] != 0 || g->sched_begin[g->n_schedulers] != g->n_units)
+    return fail(MK_ERR_CONFIG, "sched_begin does not cover the unit list");
+  if (g->n_units >= int(kEnd)) return fail(MK_ERR_CONFIG, "too many units");
+  for (int i = 0; i < g->n_tasks; ++i) {
+    const mk_task& t = g->tasks[i];
+    if (t.wait0 >= g->n_events || t.wait1 >= g->n_events || t.signal >= g->n_events)
+      return fail(MK_ERR_CONFIG, "task " + std::to_string(i) + " references an unknown event");
+    if (t.param_off < 0 || t.param_off % 8 || t.param_off > g->param_bytes)
+      return fail(MK_ERR_CONFIG, "task " + std::to_string(i) + " has a bad param offset");
+    if (t.level == MK_LEVEL_CHIPLET && (t.die < 0 || t.die >= g->n_schedulers))
+      return fail(MK_ERR_CONFIG, "chiplet task " + std::to_string(i) + " has a bad die binding");
+    if (t.n_units > 1 && (t.sub_ctr < 0 || t.sub_ctr >= g->n_sub_ctrs))
+      return fail(MK_ERR_CONFIG, "task " + std::to_string(i) + " needs a sub-counter");
+    if (t.op == MK_OP_GEMM) {
+      const mk_gemm_params* p = reinterpret_cast<const mk_gemm_params*>(
+          static_cast<const uint8_t*>(g->params) + t.param_off);
+      const int R = p->T_N * (p->epilogue == MK_EPI_SILU ? 2 : 1);
+      const int spr = p->T_K / 8;
+      if (p->T_K % 8 || p->T_K > 1024 || 256 % spr || p->K % p->T_K || size_t(R) * p->T_K * 2 > size_t(kSlotBytes) ||
+          p->N % R || p->T_M > kMaxNB || R > 32 || (p->epilogue == MK_EPI_LOGITS && p->M > kAmaxRows))
+        return fail(MK_ERR_CONFIG, "gemm task " + std::to_string(i) + " has an unsupported tile (" +
+                                       std::to_string(p->T_M) + "," + std::to_string(p->T_N) + "," +
+                                       std::to_string(p->T_K) + ")");
+    }
+    if (t.op == MK_OP_ATTN_PARTIAL || t.op == MK_OP_ATTN_REDUCE) {
+      const mk_attn_params* p = reinterpret_cast<const mk_attn_params*>(
+          static_cast<const uint8_t*>(g->params) + t.param_off);
+      const int hd = p->head_dim;
+      if ((hd != 16 && hd != 32 && hd != 64 && hd != 128) || p->group < 1 || p->group > 8 ||
+          8 % p->group || size_t(p->split) * hd * 2 > size_t(kSlotBytes))
+        return fail(MK_ERR_CONFIG, "attention task " + std::to_string(i) + " has unsupported shapes");
+    }
+  }
+  for (int u = 0; u < g->n_units; ++u)
+    if (g->units[u].task < 0 || g->units[u].task >= g->n_tasks)
+      return fail(MK_ERR_CONFIG, "unit " + std::to_string(u) + " references an unknown task");
+  return MK_OK;
+}
+
+static int reset_state(mk_handle* h) {
+  CK(cudaMemset(h->d_ev_ctr, 0, sizeof(uint32_t) * std::max(1, h->n_events)));
+  CK(cudaMemset(h->d_die_ctr, 0, sizeof(uint32_t) * std::max(1, h->n_events * h->n_sched)));
+  CK(cudaMemset(h->d_sub_ctr, 0, sizeof(uint32_t) * std::max(1, h->n_sub)));
+  CK(cudaMemset(h->d_mailbox, 0, sizeof(uint64_t) * size_t(h->n_sched) * h->W * kMailbox));
+  CK(cudaMemset(h->d_mb_head, 0, sizeof(uint64_t) * size_t(h->n_sched) * h->W));
+  CK(cudaMemset(h->d_mb_tail, 0, sizeof(uint64_t) * size_t(h->n_sched) * h->W));
+  CK(cudaMemset(h->d_role_ctr, 0, sizeof(uint32_t) * MK_MAX_DIES));
+  CK(cudaMemset(h->d_err, 0, 2 * sizeof(int)));
+  CK(cudaDeviceSynchronize());
+  h->epoch = 0;
+  return MK_OK;
+}
+
+
+int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_handle** out) {
+  if (!out || !topo) return fail(MK_ERR_CONFIG, "null argument");
+  int rc = validate_graph(g);
+  if (rc) return rc;
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (topo->num_sms != prop.multiProcessorCount)
+    return fail(MK_ERR_CONFIG, "topology was probed on a different device");
+  mk_handle* h = new mk_handle();
+  h->device = device;
+  h->num_sms = prop.multiProcessorCount;
+  h->sched_mode = g->sched_mode;
+  h->n_sched = g->n_schedulers;
+  h->W = g->workers_per_sched;
+  h->n_events = g->n_events;
+  h->n_tasks = g->n_tasks;
+  h->n_units = g->n_units;
+  h->n_sub = g->n_sub_ctrs;
+  std::vector<int8_t> die_of_sm(MK_MAX_SMS, 0);
+  h->group_size.assign(MK_MAX_DIES, 0);
+  if (g->sched_mode == MK_SCHED_FLAT) {
+    if (g->n_schedulers != 1) { delete h; return fail(MK_ERR_CONFIG, "flat mode has one scheduler"); }
+    h->group_size[0] = h->num_sms;
+    if (h->W > h->num_sms - 1) { delete h; return fail(MK_ERR_CONFIG, "more workers than SMs"); }
+  } else {
+    if (g->n_schedulers != topo->num_dies) {
+      delete h;
+      return fail(MK_ERR_CONFIG, "graph built for " + std::to_string(g->n_schedulers) +
+                                     " dies, device has " + std::to_string(topo->num_dies));
+    }
+    for (int d = 0; d < topo->num_dies; ++d) {
+      h->group_size[d] = topo->sms_per_die[d];
+      if (h->W > topo->sms_per_die[d] - 1) {
+        delete h;
+        return fail(MK_ERR_CONFIG, "die " + std::to_string(d) + " has too few SMs for W");
+      }
+    }
+    for (int i = 0; i < MK_MAX_SMS; ++i) die_of_sm[i] = int8_t(topo->die_of_sm[i]);
+  }
+#define DA(p, n) do { int r_ = dalloc(&p, n); if (r_) { delete h; return r_; } } while (0)
+  DA(h->d_tasks, g->n_tasks);
+  DA(h->d_units, g->n_units);
+  DA(h->d_sched_begin, g->n_schedulers + 1);
+  DA(h->d_params, g->param_bytes);
+  DA(h->d_ev_ctr, g->n_events);
+  DA(h->d_ev_req, g->n_events);
+  DA(h->d_die_ctr, size_t(g->n_events) * g->n_schedulers);
+  DA(h->d_sub_ctr, g->n_sub_ctrs);
+  DA(h->d_mailbox, size_t(g->n_schedulers) * h->W * kMailbox);
+  DA(h->d_mb_head, size_t(g->n_schedulers) * h->W);
+  DA(h->d_mb_tail, size_t(g->n_schedulers) * h->W);
+  DA(h->d_die_of_sm, MK_MAX_SMS);
+  DA(h->d_role_ctr, MK_MAX_DIES);
+  DA(h->d_group_size, MK_MAX_DIES);
+  DA(h->d_stats, 16);
+  DA(h->d_err, 2);
+  DA(h->d_log_cursor, 1);
+  DA(h->d_tile_cursor, 1);
+#undef DA
+  CK(cudaMallocHost(&h->h_err, 2 * sizeof(int)));
+  CK(cudaMemcpy(h->d_tasks, g->tasks, sizeof(mk_task) * g->n_tasks, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->d_units, g->units, sizeof(mk_unit) * g->n_units, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->d_sched_begin, g->sched_begin, sizeof(int32_t) * (g->n_schedulers + 1),
+                cudaMemcpyHostToDevice));
+  if (g->param_bytes)
+    CK(cudaMemcpy(h->d_params, g->params, g->param_bytes, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->d_ev_req, g->event_required, sizeof(int32_t) * g->n_events, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->d_die_of_sm, die_of_sm.data(), MK_MAX_SMS, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->d_group_size, h->group_size.data(), sizeof(int32_t) * MK_MAX_DIES,
+                cudaMemcpyHostToDevice));
+  CK(cudaMemset(h->d_stats, 0, 16 * sizeof(unsigned long long)));
+  CK(cudaMemset(h->d_log_cursor, 0, sizeof(unsigned long long)));
+  CK(cudaMemset(h->d_tile_cursor, 0, sizeof(unsigned long long)));
+  CK(cudaFuncSetAttribute(megakernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, megakernel, kThreads, kSmemBytes));
+  if (occ != 1) {
+    delete h;
+    return fail(MK_ERR_CONFIG, "megakernel occupancy is " + std::to_string(occ) + ", need exactly 1");
+  }
+  rc = reset_state(h);
+  if (rc) { delete h; return rc; }
+  *out = h;
+  return MK_OK;
+}
+
+int mk_step(mk_handle* h, void* stream) {
+  if (!h) return fail(MK_ERR_CONFIG, "null handle");
+  CK(cudaSetDevice(h->device));
+  h->epoch += 1;
+  KArgs a;
+  a.tasks = h->d_tasks; a.units = h->d_units; a.sched_begin = h->d_sched_begin;
+  a.params = h->d_params; a.ev_ctr = h->d_ev_ctr; a.ev_req = h->d_ev_req;
+  a.die_ctr = h->d_die_ctr; a.sub_ctr = h->d_sub_ctr; a.mailbox = h->d_mailbox;
+  a.mb_head = h->d_mb_head; a.mb_tail = h->d_mb_tail; a.die_of_sm = h->d_die_of_sm;
+  a.role_ctr = h->d_role_ctr; a.group_size = h->d_group_size; a.stats = h->d_stats;
+  a.log = h->log_cap ? h->d_log : nullptr; a.log_cursor = h->d_log_cursor; a.log_cap = h->log_cap;
+  a.tile_log = h->tile_cap ? h->d_tile_log : nullptr; a.tile_cursor = h->d_tile_cursor;
+  a.tile_cap = h->tile_cap;
+  a.err = h->d_err; a.err_info = h->d_err + 1;
+  a.watchdog_ns = (unsigned long long)(h->watchdog_s * 1e9);
+  a.n_events = h->n_events; a.n_sched = h->n_sched; a.sched_mode = h->sched_mode; a.W = h->W;
+  a.epoch = h->epoch;
+  void* args[] = {&a};
+  CK(cudaLaunchCooperativeKernel((const void*)megakernel, dim3(h->num_sms), dim3(kThreads), args,
+                                 kSmemBytes, static_cast<cudaStream_t>(stream)));
+  return MK_OK;
+}
+
+int mk_sync(mk_handle* h) {
+  if (!h) return fail(MK_ERR_CONFIG, "null handle");
+  CK(cudaSetDevice(h->device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(h->h_err, h->d_err, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+  if (h->h_err[0] != 0) {
+    const int code = h->h_err[0], info = h->h_err[1];
+    reset_state(h);
+    return fail(code, "device watchdog: no progress (event/site " + std::to_string(info) + ")");
+  }
+  return MK_OK;
+}
+
+int mk_counters_get(mk_handle* h, mk_counters* out) {
+  if (!h || !out) return fail(MK_ERR_CONFIG, "null argument");
+  CK(cudaSetDevice(h->device));
+  unsigned long long s[16];
+  CK(cudaMemcpy(s, h->d_stats, sizeof(s), cudaMemcpyDeviceToHost));
+  out->dispatches = s[S_DISPATCH]; out->mailbox_writes = s[S_MAILBOX];
+  out->global_atomics = s[S_GLOBAL]; out->local_atomics = s[S_LOCAL]; out->fences = s[S_FENCE];
+  out->fanout_atomics = s[S_FANOUT]; out->polls = s[S_POLL]; out->tiles = s[S_TILES];
+  out->executions = s[S_EXEC]; out->steps = s[S_STEPS];
+  return MK_OK;
+}
+
+int mk_counters_reset(mk_handle* h) {
+  if (!h) return fail(MK_ERR_CONFIG, "null handle");
+  CK(cudaSetDevice(h->device));
+  CK(cudaMemset(h->d_stats, 0, 16 * sizeof(unsigned long long)));
+  return MK_OK;
+}
+
+int mk_log_enable(mk_handle* h, int64_t capacity) {
+  if (!h) return fail(MK_ERR_CONFIG, "null handle");
+  CK(cudaSetDevice(h->device));
+  if (h->d_log) { CK(cudaFree(h->d_log)); h->d_log = nullptr; }
+  h->log_cap = 0;
+  if (capacity > 0) {
+    CK(cudaMalloc(&h->d_log, sizeof(mk_log_rec) * capacity));
+    h->log_cap = capacity;
+  }
+  CK(cudaMemset(h->d_log_cursor, 0, sizeof(unsigned long long)));
+  return MK_OK;
+}
+
+int64_t mk_log_read(mk_handle* h, mk_log_rec* out, int64_t max_records) {
+  if (!h || !out) return -fail(MK_ERR_CONFIG, "null argument");
+  if (cudaSetDevice(h->device) != cudaSuccess) return -MK_ERR_CUDA;
+  unsigned long long n = 0;
+  if (cudaMemcpy(&n, h->d_log_cursor, sizeof(n), cudaMemcpyDeviceToHost) != cudaSuccess) return -MK_ERR_CUDA;
+  long long m = std::min<long long>((long long)n, std::min<long long>(h->log_cap, max_records));
+  if (m > 0 && cudaMemcpy(out, h->d_log, sizeof(mk_log_rec) * m, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -MK_ERR_CUDA;
+  return (int64_t)n;
+}
+
+int mk_tile_log_enable(mk_handle* h, int64_t capacity) {
+  if (!h) return fail(MK_ERR_CONFIG, "null handle");
+  CK(cudaSetDevice(h->device));
+  if (h->d_tile_log) { CK(cudaFree(h->d_tile_log)); h->d_tile_log = nullptr; }
+  h->tile_cap = 0;
+  if (capacity > 0) {
+    CK(cudaMalloc(&h->d_tile_log, sizeof(int32_t) * 4 * capacity));
+    h->tile_cap = capacity;
+  }
+  CK(cudaMemset(h->d_tile_cursor, 0, sizeof(unsigned long long)));
+  return MK_OK;
+}
+
+int64_t mk_tile_log_read(mk_handle* h, int32_t* out4, int64_t max_records) {
+  if (!h || !out4) return -fail(MK_ERR_CONFIG, "null argument");
+  if (cudaSetDevice(h->device) != cudaSuccess) return -MK_ERR_CUDA;
+  unsigned long long n = 0;
+  if (cudaMemcpy(&n, h->d_tile_cursor, sizeof(n), cudaMemcpyDeviceToHost) != cudaSuccess) return -MK_ERR_CUDA;
+  long long m = std::min<long long>((long long)n, std::min<long long>(h->tile_cap, max_records));
+  if (m > 0 && cudaMemcpy(out4, h->d_tile_log, sizeof(int32_t) * 4 * m, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -MK_ERR_CUDA;
+  return (int64_t)n;
+}
+
+int mk_set_watchdog(mk_handle* h, double seconds) {
+  if (!h || !(seconds > 0)) return fail(MK_ERR_CONFIG, "bad watchdog");
+  h->watchdog_s = seconds;
+  return MK_OK;
+}
+
+int mk_destroy(mk_handle* h) {
+  if (!h) return MK_OK;
+  cudaSetDevice(h->device);
+  cudaFree(h->d_tasks); cudaFree(h->d_units); cudaFree(h->d_sched_begin); cudaFree(h->d_params);
+  cudaFree(h->d_ev_ctr); cudaFree(h->d_ev_req); cudaFree(h->d_die_ctr); cudaFree(h->d_sub_ctr);
+  cudaFree(h->d_mailbox); cudaFree(h->d_mb_head); cudaFree(h->d_mb_tail); cudaFree(h->d_die_of_sm);
+  cudaFree(h->d_role_ctr); cudaFree(h->d_group_size); cudaFree(h->d_stats); cudaFree(h->d_err);
+  cudaFree(h->d_log); cudaFree(h->d_log_cursor); cudaFree(h->d_tile_log); cudaFree(h->d_tile_cursor);
+  if (h->h_err) cudaFreeHost(h->h_err);
+  delete h;
+  return MK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,376 @@
+"""Host graph compiler: TaskGraph -> flat device descriptor arrays.
+
+Input: a graph from :func:`.taskgraph.build_decoder_layer` (the reference's
+topology, ref taskgraph.py:355-526) plus the device buffers of one model
+instance.  Output: the arrays of ``mk_graph_desc`` (include/mk.h):
+
+* one ``mk_task`` per graph task, in graph order, with the event it waits
+  on, the event it signals and an op parameter block (device pointers,
+  shapes, tile, traversal / distribution);
+* three appended stages the reference graph lacks (SURVEY.md section 7.3 item
+  9): ``final_norm`` -> ``lm_head`` -> ``argmax``, so one launch produces
+  greedy token ids;
+* the per-scheduler dispatch lists in topological (graph) order: a die task
+  goes to its die's list, CU task units go round-robin across dies in graph
+  order -- the reference's ``enqueue`` rule (ref runtime.py:301-307);
+* event ``required_count`` (ref taskgraph.py:221) and sub-counters for CU
+  tasks whose items are fanned out over several workers (attention, norms):
+  the fanned task still signals its event exactly once.
+
+The reference work payloads (GemmWork / GemmTileWork / ElementwiseWork) are
+mapped to real pointers: weights are packed tile-major per op
+(weights.pack_tiles), a die task's slab pointer is the reference's
+``weight_base + x*K*N_local*dtype`` (taskgraph.py:330) realised on the packed
+tensor, and its output block starts at column ``x*N_local``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+from . import _lib as L
+from .taskgraph import OpKind, TaskGraph, TaskLevel
+from .traversal import Distribution, Traversal
+
+
+def _cdiv(a, b):
+    return (a + b - 1) // b
+
+
+@dataclass
+class LoweringOptions:
+    sched_mode: int = L.SCHED_PER_DIE
+    traversal: Traversal = Traversal.M_MAJOR_WINDOWED
+    distribution: Distribution = Distribution.M_TILE
+    workers: int = 73              # W per scheduler
+    n_dies: int = 2                # schedulers in PER_DIE mode
+    fanout: bool = True            # split CU tasks' items over several units
+    lm_tile: tuple = (16, 8, 1024)  # (T_M, T_N, T_K) of the appended LM head
+    attn_split: int = 64           # tokens per split-KV item
+
+
+@dataclass
+class Lowered:
+    tasks: object
+    units: object
+    sched_begin: object
+    event_required: object
+    params: bytes
+    event_names: list
+    task_names: list
+    graph_task_index: list
+    n_sub: int
+    n_sched: int
+    sched_mode: int
+    workers: int
+    amax_slots: int
+    keep: list = field(default_factory=list)   # ctypes arrays kept alive
+
+    def desc(self) -> L.GraphDesc:
+        pbuf = C.create_string_buffer(self.params, max(1, len(self.params)))
+        self.keep.append(pbuf)
+        g = L.GraphDesc()
+        g.n_tasks = len(self.tasks)
+        g.n_events = len(self.event_required)
+        g.n_units = len(self.units)
+        g.n_sub_ctrs = self.n_sub
+        g.n_schedulers = self.n_sched
+        g.sched_mode = self.sched_mode
+        g.workers_per_sched = self.workers
+        g.param_bytes = len(self.params)
+        g.tasks = C.cast(self.tasks, C.c_void_p)
+        g.event_required = C.cast(self.event_required, C.c_void_p)
+        g.units = C.cast(self.units, C.c_void_p)
+        g.sched_begin = C.cast(self.sched_begin, C.c_void_p)
+        g.params = C.cast(pbuf, C.c_void_p)
+        return g
+
+
+class _Blob:
+    def __init__(self):
+        self.data = bytearray()
+
+    def add(self, struct) -> int:
+        off = len(self.data)
+        self.data += bytes(struct)
+        while len(self.data) % 8:
+            self.data += b"\0"
+        return off
+
+
+def _ptr(t, elem_offset=0):
+    if t is None:
+        return None
+    return t.data_ptr() + elem_offset * t.element_size()
+
+
+def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
+    """Lower ``g`` against device buffers ``bufs`` (a runtime.DeviceState)."""
+    B = g.batch
+    d, F, hd = spec.hidden, spec.ffn, spec.head_dim
+    per_die = opts.sched_mode == L.SCHED_PER_DIE
+    n_sched = opts.n_dies if per_die else 1
+    if not per_die:
+        for t in g.tasks:
+            if t.level is TaskLevel.CHIPLET and t.xcd_binding != 0:
+                raise ValueError("the flat scheduler runs die-unaware graphs "
+                                 "(standard mode or a 1-die machine)")
+    blob = _Blob()
+    event_names = list(g.events)
+    ev_index = {e: i for i, e in enumerate(event_names)}
+    required = [g.events[e].required_count for e in event_names]
+    tasks, names, gidx = [], [], []
+    units_by_sched = [[] for _ in range(n_sched)]
+    rr = [0]
+    n_sub = [0]
+    total_workers = opts.workers * n_sched
+    trav = L.TRAV_M_MAJOR if opts.traversal is Traversal.M_MAJOR_WINDOWED \
+        else L.TRAV_N_MAJOR
+    dist = L.DIST_M_SPLIT if opts.distribution is Distribution.M_SPLIT \
+        else L.DIST_M_TILE
+
+    def add_task(name, graph_i, op, level, die, wait, signal, param_off,
+                 layer, n_items=1, n_units=1):
+        t = L.Task()
+        t.op, t.level = op, level
+        t.die = -1 if die is None else die
+        t.wait0 = -1 if wait is None else ev_index[wait]
+        t.wait1 = -1
+        t.signal = -1 if signal is None else ev_index[signal]
+        n_units = max(1, min(n_units, n_items)) if opts.fanout else 1
+        t.n_items, t.n_units = n_items, n_units
+        t.sub_ctr = -1
+        if n_units > 1:
+            t.sub_ctr = n_sub[0]
+            n_sub[0] += 1
+        t.param_off, t.layer, t.graph_index = param_off, layer, graph_i
+        ti = len(tasks)
+        tasks.append(t)
+        names.append(name)
+        gidx.append(graph_i)
+        if level == L.LEVEL_CHIPLET:
+            units_by_sched[die if per_die else 0].append((ti, 0, 0))
+        else:
+            for u in range(n_units):
+                ib = u * n_items // n_units
+                ie = (u + 1) * n_items // n_units
+                s = (rr[0] % n_sched) if per_die else 0
+                rr[0] += 1
+                units_by_sched[s].append((ti, ib, ie))
+        return ti
+
+    def gemm_params(w, x, y, res, M, K, N, tile, ldx, ldy, ldres, col0, epi,
+                    xcd, tm=-1, tn=-1, amax_base=0):
+        p = L.GemmParams()
+        p.w, p.x, p.y, p.res = w, x, y, res
+        p.amax_val = _ptr(bufs.amax_val)
+        p.amax_idx = _ptr(bufs.amax_idx)
+        p.M, p.K, p.N = M, K, N
+        p.T_M, p.T_N, p.T_K = tile
+        p.ldx, p.ldy, p.ldres, p.y_col0 = ldx, ldy, ldres, col0
+        p.epilogue, p.traversal, p.distribution, p.xcd = epi, trav, dist, xcd
+        p.tile_m, p.tile_n = tm, tn
+        p.amax_base, p.amax_stride = amax_base, B
+        return blob.add(p)
+
+    def norm_params(layer_bufs, x, gamma, y, embed=False):
+        p = L.NormParams()
+        p.x, p.gamma, p.y = _ptr(x), _ptr(gamma), _ptr(y)
+        if embed:
+            p.embed = _ptr(bufs.embed)
+            p.tokens = _ptr(bufs.tokens)
+            p.x_store = _ptr(bufs.x_in0)
+        p.M, p.d, p.eps = B, d, spec.eps
+        return blob.add(p)
+
+    def attn_params(layer, h, out=None):
+        lb = bufs.layers[layer]
+        p = L.AttnParams()
+        p.qkv = _ptr(lb["qkv_out"])
+        p.q_gamma = _ptr(bufs.w_layers[layer]["q_norm"])
+        p.k_gamma = _ptr(bufs.w_layers[layer]["k_norm"])
+        p.k_cache, p.v_cache = _ptr(bufs.k_cache[layer]), _ptr(bufs.v_cache[layer])
+        p.rope_cos, p.rope_sin = _ptr(bufs.rope_cos), _ptr(bufs.rope_sin)
+        p.positions = _ptr(bufs.positions)
+        p.partial = _ptr(bufs.partial)
+        p.out = _ptr(out)
+        p.M, p.ldqkv = B, spec.qkv_dim
+        p.q_heads, p.kv_heads, p.head_dim = spec.q_heads, spec.kv_heads, hd
+        p.group, p.kv_head = spec.group, h
+        p.split, p.n_splits, p.t_max = bufs.split, bufs.n_splits, bufs.t_max
+        p.eps, p.scale = spec.eps, hd ** -0.5
+        return blob.add(p)
+
+    u_attn = _cdiv(total_workers, spec.kv_heads)
+    u_rows = min(B, 16)
+    silu_meta = _silu_meta(g, B, F)
+
+    for gi, t in enumerate(g.tasks):
+        layer = int(t.id.split(".")[0][1:])
+        lb = bufs.layers[layer]
+        wl = bufs.w_layers[layer]
+        wait = t.wait_events[0] if t.wait_events else None
+        level = {TaskLevel.CHIPLET: L.LEVEL_CHIPLET, TaskLevel.CU: L.LEVEL_CU,
+                 TaskLevel.WAVEFRONT: L.LEVEL_WAVEFRONT}[t.level]
+        op = t.op_kind
+        if op is OpKind.RMS_NORM:
+            first = t.id.endswith("rms1.t0")
+            if first:
+                src = bufs.x_in0 if layer == 0 else bufs.layers[layer - 1]["x_out"]
+                po = norm_params(lb, src, wl["in_norm"], lb["normed1"],
+                                 embed=(layer == 0))
+            else:
+                po = norm_params(lb, lb["x_mid"], wl["post_norm"], lb["normed2"])
+            add_task(t.id, gi, L.OP_RMSNORM, level, None, wait, t.signal_event,
+                     po, layer, n_items=B, n_units=u_rows)
+        elif op in (OpKind.QKV_PROJ, OpKind.O_PROJ_RESIDUAL,
+                    OpKind.GATE_UP_SILU, OpKind.DOWN_PROJ_RESIDUAL):
+            M, K, N = t.gemm_shape
+            tile = tuple(t.tile_shape)
+            x_in = bufs.x_in0 if layer == 0 else bufs.layers[layer - 1]["x_out"]
+            if op is OpKind.QKV_PROJ:
+                w, x, y, res, epi, ldx, ldy = (bufs.w_packed[layer]["qkv"],
+                                              lb["normed1"], lb["qkv_out"], None,
+                                              L.EPI_NONE, d, spec.qkv_dim)
+            elif op is OpKind.O_PROJ_RESIDUAL:
+                w, x, y, res, epi, ldx, ldy = (bufs.w_packed[layer]["o"],
+                                              lb["attn_out"], lb["x_mid"], x_in,
+                                              L.EPI_RESIDUAL, d, d)
+            elif op is OpKind.GATE_UP_SILU:
+                fused = t.level is TaskLevel.CHIPLET
+                w = bufs.w_packed[layer]["gate_up"]
+                x, ldx = lb["normed2"], d
+                if fused:
+                    y, epi, ldy = lb["silu_out"], L.EPI_SILU, F
+                else:
+                    y, epi, ldy = lb["gu_out"], L.EPI_NONE, 2 * F
+                res = None
+            else:
+                w, x, y, res, epi, ldx, ldy = (bufs.w_packed[layer]["down"],
+                                              lb["silu_out"], lb["x_out"],
+                                              lb["x_mid"], L.EPI_RESIDUAL, F, d)
+            if t.level is TaskLevel.CHIPLET:
+                X = g.machine.num_xcds
+                n_loc = N // X
+                xd = t.xcd_binding
+                col0 = xd * (n_loc // 2 if epi == L.EPI_SILU else n_loc)
+                po = gemm_params(_ptr(w, xd * n_loc * K), _ptr(x), _ptr(y),
+                                 _ptr(res), M, K, n_loc, tile, ldx, ldy, d,
+                                 col0, epi, xd)
+                add_task(t.id, gi, L.OP_GEMM, level, xd, wait, t.signal_event,
+                         po, layer, n_items=0)
+            else:
+                work = t.work
+                po = gemm_params(_ptr(w), _ptr(x), _ptr(y), _ptr(res), M, K, N,
+                                 tile, ldx, ldy, d, 0, epi, 0,
+                                 tm=work.m_idx, tn=work.n_idx)
+                add_task(t.id, gi, L.OP_GEMM, level, None, wait, t.signal_event,
+                         po, layer)
+        elif op is OpKind.ATTN_PARTIAL:
+            h = int(t.id.rsplit(".t", 1)[1])
+            po = attn_params(layer, h)
+            add_task(t.id, gi, L.OP_ATTN_PARTIAL, level, None, wait,
+                     t.signal_event, po, layer, n_items=B * bufs.n_splits,
+                     n_units=u_attn)
+        elif op is OpKind.ATTN_REDUCE:
+            h = int(t.id.rsplit(".t", 1)[1])
+            po = attn_params(layer, h, out=lb["attn_out"])
+            add_task(t.id, gi, L.OP_ATTN_REDUCE, level, None, wait,
+                     t.signal_event, po, layer, n_items=B, n_units=u_attn)
+        elif op is OpKind.SILU:
+            row0, rows, col0, cols = silu_meta[t.id]
+            p = L.SiluParams()
+            p.gu, p.y = _ptr(lb["gu_out"]), _ptr(lb["silu_out"])
+            p.F, p.row0, p.rows, p.col0, p.cols = F, row0, rows, col0, cols
+            add_task(t.id, gi, L.OP_SILU, level, None, wait, t.signal_event,
+                     blob.add(p), layer)
+        else:
+            raise ValueError(f"cannot lower {op}")
+
+    # ---- appended stages: final norm -> LM head -> argmax ---------------
+    last_event = g.tasks[-1].signal_event
+    n_layers = len(bufs.layers)
+    for e in ("e.final_norm", "e.lm_head", "e.argmax"):
+        ev_index[e] = len(event_names)
+        event_names.append(e)
+        required.append(0)
+    po = norm_params(None, bufs.layers[n_layers - 1]["x_out"], bufs.final_norm,
+                     bufs.final_normed)
+    add_task("final_norm.t0", -1, L.OP_RMSNORM, L.LEVEL_CU, None, last_event,
+             "e.final_norm", po, n_layers, n_items=B, n_units=u_rows)
+    required[ev_index["e.final_norm"]] = 1
+    t_m, t_n, t_k = opts.lm_tile
+    V = spec.vocab
+    logits = bufs.logits
+    if per_die:
+        X = opts.n_dies
+        n_loc = V // X
+        for xd in range(X):
+            po = gemm_params(_ptr(bufs.lm_packed, xd * n_loc * d),
+                             _ptr(bufs.final_normed), _ptr(logits), None,
+                             B, d, n_loc, (t_m, t_n, t_k), d, V, d,
+                             xd * n_loc, L.EPI_LOGITS, xd,
+                             amax_base=xd * opts.workers)
+            add_task(f"lm_head.x{xd}", -1, L.OP_GEMM, L.LEVEL_CHIPLET, xd,
+                     "e.final_norm", "e.lm_head", po, n_layers, n_items=0)
+        required[ev_index["e.lm_head"]] = X
+        amax_slots = X * opts.workers
+    else:
+        mt, nt = _cdiv(B, t_m), V // t_n
+        for m in range(mt):
+            for n in range(nt):
+                po = gemm_params(_ptr(bufs.lm_packed), _ptr(bufs.final_normed),
+                                 _ptr(logits), None, B, d, V, (t_m, t_n, t_k),
+                                 d, V, d, 0, L.EPI_LOGITS, 0, tm=m, tn=n,
+                                 amax_base=n)
+                add_task(f"lm_head.t{m * nt + n}", -1, L.OP_GEMM, L.LEVEL_CU,
+                         None, "e.final_norm", "e.lm_head", po, n_layers)
+        required[ev_index["e.lm_head"]] = mt * nt
+        amax_slots = nt
+    p = L.ArgmaxParams()
+    p.amax_val, p.amax_idx = _ptr(bufs.amax_val), _ptr(bufs.amax_idx)
+    p.out_tokens, p.next_tokens = _ptr(bufs.out_tokens), _ptr(bufs.tokens)
+    p.positions = _ptr(bufs.positions)
+    p.M, p.n_slots = B, amax_slots
+    add_task("argmax.t0", -1, L.OP_ARGMAX, L.LEVEL_CU, None, "e.lm_head",
+             "e.argmax", blob.add(p), n_layers, n_items=B, n_units=u_rows)
+    required[ev_index["e.argmax"]] = 1
+
+    flat_units = [u for s in units_by_sched for u in s]
+    begin = [0]
+    for s in units_by_sched:
+        begin.append(begin[-1] + len(s))
+    t_arr = (L.Task * len(tasks))(*tasks)
+    u_arr = (L.Unit * len(flat_units))(
+        *[L.Unit(ti, ib, ie, 0) for ti, ib, ie in flat_units])
+    b_arr = (C.c_int32 * len(begin))(*begin)
+    r_arr = (C.c_int32 * len(required))(*required)
+    return Lowered(t_arr, u_arr, b_arr, r_arr, bytes(blob.data), event_names,
+                   names, gidx, n_sub[0], n_sched, opts.sched_mode,
+                   opts.workers, amax_slots)
+
+
+def _silu_meta(g: TaskGraph, B: int, F: int):
+    """(row0, rows, col0, cols) of every standard-mode SiLU task
+    (ref taskgraph.py:476-504: ids t{group*n_chunks + chunk})."""
+    out = {}
+    by_layer = {}
+    for t in g.tasks:
+        if t.op_kind is OpKind.SILU:
+            by_layer.setdefault(t.id.split(".")[0], []).append(t)
+    for tasks in by_layer.values():
+        gu = [t for t in g.tasks if t.op_kind is OpKind.GATE_UP_SILU][0]
+        t_m = gu.tile_shape[0]
+        groups = _cdiv(B, t_m)
+        n_chunks = len(tasks) // groups
+        dt = 2
+        first_rows = min(t_m, B)
+        chunk = tasks[0].work.reads[0][1] // (first_rows * dt)
+        for t in tasks:
+            k = int(t.id.rsplit(".t", 1)[1])
+            grp, j = divmod(k, n_chunks)
+            rows = min(t_m, B - grp * t_m)
+            cols = min(chunk, F - j * chunk)
+            out[t.id] = (grp * t_m, rows, j * chunk, cols)
+    return out

@@ -1,0 +1,380 @@
+"""Device runtime: the B200 replacement of the reference's ``simulate``.
+
+The reference executes a TaskGraph with ``simulate(g, machine, h, *,
+traversal, distribution, ...)`` (``runtime.py:253-548``), a Python model of a
+persistent kernel.  Here the same graph is lowered (:mod:`.lowering`) and
+executed by the real persistent kernel through the C ABI (``include/mk.h``):
+
+    topo = probe()                       # dies from %smid latency clustering
+    machine = b200_from_probe(topo.sms_per_die)
+    g = build_decoder_layer(model, machine, "chiplet", batch, tiles, layers)
+    mk = Megakernel(g, weights, ctx=1024, traversal=..., distribution=...)
+    tokens = mk.step()                   # one launch = one decode step
+
+:func:`run` is the drop-in shaped like ``simulate``: it returns a
+:class:`DeviceTrace` with the reference counter names (fences,
+global_atomics, local_atomics, dispatches, polls) and the event log
+(``(step, actor, action, task_id)``, runtime.py:326-477).
+
+There is no CPU path: constructing a Megakernel without a GPU or without
+``libmk.so`` raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib as L
+from .lowering import LoweringOptions, lower
+from .machine import b200_from_probe
+from .taskgraph import OpKind, TaskGraph, TaskLevel
+from .traversal import Distribution, Traversal
+from .weights import (Qwen3Spec, Qwen3Weights, hash_uniform, pack_gate_up_fused,
+                      pack_tiles, rope_tables)
+
+
+def probe(device: int = 0) -> L.Topology:
+    """Measure the die map of ``device`` (mk_probe)."""
+    lib = L.load()
+    topo = L.Topology()
+    L.check(lib.mk_probe(device, C.byref(topo)))
+    return topo
+
+
+def topology_summary(topo: L.Topology) -> dict:
+    return {
+        "num_sms": topo.num_sms,
+        "num_dies": topo.num_dies,
+        "sms_per_die": [topo.sms_per_die[i] for i in range(topo.num_dies)],
+        "separation": round(float(topo.separation), 3),
+        "near_cycles": round(float(topo.near_cycles), 1),
+        "far_cycles": round(float(topo.far_cycles), 1),
+    }
+
+
+def halves_topology(num_sms: int) -> L.Topology:
+    """Fallback split by smid halves (used only when the probe cannot
+    separate the dies; reported as separation 0)."""
+    t = L.Topology()
+    t.num_sms = num_sms
+    t.num_dies = 2
+    t.sms_per_die[0] = num_sms // 2
+    t.sms_per_die[1] = num_sms - num_sms // 2
+    for i in range(num_sms):
+        t.die_of_sm[i] = 0 if i < num_sms // 2 else 1
+    return t
+
+
+def flat_topology(num_sms: int) -> L.Topology:
+    t = L.Topology()
+    t.num_sms = num_sms
+    t.num_dies = 1
+    t.sms_per_die[0] = num_sms
+    return t
+
+
+def _graph_tiles(g: TaskGraph):
+    tiles = {}
+    for t in g.tasks:
+        if t.tile_shape and t.op_kind not in tiles:
+            tiles[t.op_kind] = tuple(t.tile_shape)
+    return tiles
+
+
+@dataclass
+class DeviceState:
+    """Every device buffer one graph instance touches (borrowed by the kernel)."""
+
+    spec: Qwen3Spec
+    batch: int
+    t_max: int
+    split: int
+    n_splits: int
+    embed: torch.Tensor = None
+    final_norm: torch.Tensor = None
+    lm_packed: torch.Tensor = None
+    w_packed: list = field(default_factory=list)
+    w_layers: list = field(default_factory=list)
+    layers: list = field(default_factory=list)
+    k_cache: list = field(default_factory=list)
+    v_cache: list = field(default_factory=list)
+    x_in0: torch.Tensor = None
+    final_normed: torch.Tensor = None
+    logits: torch.Tensor = None
+    amax_val: torch.Tensor = None
+    amax_idx: torch.Tensor = None
+    partial: torch.Tensor = None
+    tokens: torch.Tensor = None
+    out_tokens: torch.Tensor = None
+    positions: torch.Tensor = None
+    rope_cos: torch.Tensor = None
+    rope_sin: torch.Tensor = None
+
+
+def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
+                amax_slots: int, device="cuda", split: int | None = None,
+                keep_logits: bool = True) -> DeviceState:
+    sp = weights.spec
+    B = g.batch
+    dev = torch.device(device)
+    hd = sp.head_dim
+    split = split or max(8, 8192 // hd)
+    n_splits = (t_max + split - 1) // split
+    st = DeviceState(sp, B, t_max, split, n_splits)
+    w = weights.to(dev)
+    tiles = _graph_tiles(g)
+    chiplet = g.mode == "chiplet"
+    X = g.machine.num_xcds
+    bf = dict(device=dev, dtype=torch.bfloat16)
+    n_layers = len(g.buffers)
+    for li in range(n_layers):
+        Lw = w.layers[li]
+        qkv = torch.cat((Lw["q"], Lw["k"], Lw["v"]), 0)
+        _, tn, tk = tiles[OpKind.QKV_PROJ]
+        packed = {"qkv": pack_tiles(qkv, tn, tk)}
+        _, tn, tk = tiles[OpKind.O_PROJ_RESIDUAL]
+        packed["o"] = pack_tiles(Lw["o"], tn, tk)
+        _, tn, tk = tiles[OpKind.GATE_UP_SILU]
+        if chiplet:
+            packed["gate_up"] = pack_gate_up_fused(Lw["gate"], Lw["up"], X, tn, tk)
+        else:
+            packed["gate_up"] = pack_tiles(torch.cat((Lw["gate"], Lw["up"]), 0), tn, tk)
+        _, tn, tk = tiles[OpKind.DOWN_PROJ_RESIDUAL]
+        packed["down"] = pack_tiles(Lw["down"], tn, tk)
+        st.w_packed.append(packed)
+        st.w_layers.append({k: Lw[k] for k in ("q_norm", "k_norm", "in_norm", "post_norm")})
+        st.layers.append({
+            "normed1": torch.zeros(B, sp.hidden, **bf),
+            "qkv_out": torch.zeros(B, sp.qkv_dim, **bf),
+            "attn_out": torch.zeros(B, sp.hidden, **bf),
+            "x_mid": torch.zeros(B, sp.hidden, **bf),
+            "normed2": torch.zeros(B, sp.hidden, **bf),
+            "gu_out": torch.zeros(B, 2 * sp.ffn, **bf) if not chiplet else None,
+            "silu_out": torch.zeros(B, sp.ffn, **bf),
+            "x_out": torch.zeros(B, sp.hidden, **bf),
+        })
+        st.k_cache.append(torch.zeros(B, sp.kv_heads, t_max, hd, **bf))
+        st.v_cache.append(torch.zeros(B, sp.kv_heads, t_max, hd, **bf))
+    del w.layers[:]
+    _, tn, tk = lm_tile
+    st.lm_packed = pack_tiles(w.lm_head, tn, tk)
+    st.embed = w.embed
+    st.final_norm = w.final_norm
+    st.x_in0 = torch.zeros(B, sp.hidden, **bf)
+    st.final_normed = torch.zeros(B, sp.hidden, **bf)
+    st.logits = torch.zeros(B, sp.vocab, device=dev, dtype=torch.float32) \
+        if keep_logits else None
+    st.amax_val = torch.zeros(amax_slots, B, device=dev, dtype=torch.float32)
+    st.amax_idx = torch.zeros(amax_slots, B, device=dev, dtype=torch.int32)
+    st.partial = torch.zeros(B * sp.kv_heads * n_splits * sp.group * (hd + 4),
+                             device=dev, dtype=torch.float32)
+    st.tokens = torch.zeros(B, device=dev, dtype=torch.int32)
+    st.out_tokens = torch.zeros(B, device=dev, dtype=torch.int32)
+    st.positions = torch.zeros(B, device=dev, dtype=torch.int32)
+    cos, sin = rope_tables(hd, sp.rope_theta, t_max)
+    st.rope_cos, st.rope_sin = cos.to(dev), sin.to(dev)
+    return st
+
+
+class Megakernel:
+    """One lowered graph bound to one device: ``step()`` = one decode step."""
+
+    def __init__(self, g: TaskGraph, weights: Qwen3Weights, *, t_max: int,
+                 traversal: Traversal = Traversal.M_MAJOR_WINDOWED,
+                 distribution: Distribution = Distribution.M_TILE,
+                 sched: str = "per_die", topo: L.Topology | None = None,
+                 fanout: bool = True, lm_tile=None, device: int = 0,
+                 keep_logits: bool = True, watchdog_s: float = 10.0):
+        if not torch.cuda.is_available():
+            raise RuntimeError("Megakernel needs a CUDA device (no CPU fallback)")
+        self.lib = L.load()
+        torch.cuda.set_device(device)
+        self.device = device
+        self.graph = g
+        self.spec = weights.spec
+        if topo is None:
+            topo = probe(device)
+        self.topo = topo
+        per_die = sched == "per_die"
+        if per_die:
+            workers = g.machine.workers_per_xcd
+            n_dies = g.machine.num_xcds
+        else:
+            workers = topo.num_sms - 1
+            n_dies = 1
+        if lm_tile is None:
+            lm_tile = _default_lm_tile(self.spec, g.batch)
+        opts = LoweringOptions(
+            sched_mode=L.SCHED_PER_DIE if per_die else L.SCHED_FLAT,
+            traversal=traversal, distribution=distribution, workers=workers,
+            n_dies=n_dies, fanout=fanout, lm_tile=lm_tile)
+        amax_slots = (n_dies * workers) if per_die else \
+            self.spec.vocab // lm_tile[1]
+        self.state = build_state(g, weights, t_max, lm_tile, amax_slots,
+                                 device=f"cuda:{device}",
+                                 keep_logits=keep_logits)
+        self.lowered = lower(g, self.spec, self.state, opts)
+        run_topo = topo if per_die else flat_topology(topo.num_sms)
+        self._desc = self.lowered.desc()
+        h = C.c_void_p()
+        L.check(self.lib.mk_create(device, C.byref(self._desc), C.byref(run_topo),
+                                   C.byref(h)))
+        self.h = h
+        L.check(self.lib.mk_set_watchdog(self.h, watchdog_s))
+        self.steps = 0
+
+    # ---- state -----------------------------------------------------------
+    def set_tokens(self, tokens):
+        self.state.tokens.copy_(torch.as_tensor(tokens, dtype=torch.int32))
+
+    def set_positions(self, positions):
+        self.state.positions.copy_(torch.as_tensor(positions, dtype=torch.int32))
+
+    def fill_kv_random(self, n_tokens: int, seed: int = 99):
+        """Perf runs: ``n_tokens`` of synthetic bf16 context per sequence."""
+        for li, (k, v) in enumerate(zip(self.state.k_cache, self.state.v_cache)):
+            for j, buf in enumerate((k, v)):
+                n = buf[:, :, :n_tokens].numel()
+                u = hash_uniform(n, seed, 2 * li + j, device=buf.device)
+                buf[:, :, :n_tokens] = ((u * 2 - 1) * 1.7).to(torch.bfloat16).view(
+                    buf[:, :, :n_tokens].shape)
+        self.set_positions([n_tokens] * self.graph.batch)
+
+    # ---- execution ---------------------------------------------------------
+    def launch(self, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        L.check(self.lib.mk_step(self.h, C.c_void_p(s.cuda_stream)))
+        self.steps += 1
+
+    def sync(self):
+        L.check(self.lib.mk_sync(self.h))
+
+    def step(self, tokens=None):
+        """One decode step; returns the greedy tokens (int32 [B], on device)."""
+        if tokens is not None:
+            self.set_tokens(tokens)
+        self.launch()
+        self.sync()
+        return self.state.out_tokens.clone()
+
+    def logits(self):
+        return self.state.logits
+
+    def counters(self) -> dict:
+        c = L.Counters()
+        L.check(self.lib.mk_counters_get(self.h, C.byref(c)))
+        return c.as_dict()
+
+    def reset_counters(self):
+        L.check(self.lib.mk_counters_reset(self.h))
+
+    def enable_log(self, capacity: int):
+        L.check(self.lib.mk_log_enable(self.h, capacity))
+
+    def read_log(self, capacity: int):
+        buf = (L.LogRec * capacity)()
+        n = self.lib.mk_log_read(self.h, buf, capacity)
+        if n < 0:
+            L.check(-n)
+        return [buf[i] for i in range(min(n, capacity))], n
+
+    def enable_tile_log(self, capacity: int):
+        L.check(self.lib.mk_tile_log_enable(self.h, capacity))
+
+    def read_tile_log(self, capacity: int):
+        buf = (C.c_int32 * (4 * capacity))()
+        n = self.lib.mk_tile_log_read(self.h, buf, capacity)
+        if n < 0:
+            L.check(-n)
+        m = min(n, capacity)
+        return [tuple(buf[4 * i:4 * i + 4]) for i in range(m)], n
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.mk_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _default_lm_tile(spec: Qwen3Spec, batch: int):
+    t_k = 1024 if spec.hidden % 1024 == 0 else spec.hidden
+    t_k = min(t_k, 1024)
+    t_n = max(1, min(32, 8192 // t_k))
+    while spec.vocab % (2 * t_n):
+        t_n //= 2
+    return (16, t_n, t_k)
+
+
+@dataclass
+class DeviceTrace:
+    """simulate()-shaped result of device runs (ref runtime.py:92-171)."""
+
+    mode: str
+    batch: int
+    traversal: str
+    distribution: str
+    steps: int
+    fences_issued: int
+    global_atomics: int
+    local_atomics: int
+    poll_count: int
+    dispatches: int
+    counters: dict
+    event_log: tuple
+
+
+def run(g: TaskGraph, weights: Qwen3Weights, *, t_max: int, steps: int = 1,
+        traversal=Traversal.M_MAJOR_WINDOWED,
+        distribution=Distribution.M_TILE, sched: str = "per_die",
+        keep_event_log: bool = True, fanout: bool = True,
+        topo=None) -> DeviceTrace:
+    """Execute ``steps`` decode steps of ``g`` on the GPU (drop-in for simulate)."""
+    mk = Megakernel(g, weights, t_max=t_max, traversal=traversal,
+                    distribution=distribution, sched=sched, fanout=fanout,
+                    topo=topo)
+    cap = 0
+    if keep_event_log:
+        cap = 4 * (len(mk.lowered.units) * (g.machine.workers_per_xcd + 1)) + 1024
+        mk.enable_log(cap)
+    for _ in range(steps):
+        mk.step()
+    c = mk.counters()
+    log = ()
+    if keep_event_log:
+        recs, _ = mk.read_log(cap)
+        log = tuple(device_log_to_reference(mk, recs))
+    tr = DeviceTrace(g.mode, g.batch, traversal.value, distribution.value,
+                     steps, c["fences"], c["global_atomics"], c["local_atomics"],
+                     c["polls"], c["dispatches"], c, log)
+    mk.close()
+    return tr
+
+
+def device_log_to_reference(mk: Megakernel, recs):
+    """Device records -> the reference's (time, actor, action, task_id) tuples.
+
+    Dispatch records come from the scheduler CTAs (actor ``sched.x{die}``),
+    execution records from workers (``worker.x{die}.w{w}``).  Time is the
+    %globaltimer nanosecond stamp (the reference's logical ``step``).
+    """
+    names = mk.lowered.task_names
+    W = mk.lowered.workers
+    out = []
+    for r in sorted(recs, key=lambda r: (r.t_start, r.kind)):
+        if r.kind == 0:
+            out.append((int(r.t_start), f"sched.x{-1 - r.worker}", "dispatch",
+                        names[r.task]))
+        else:
+            out.append((int(r.t_start), f"worker.x{r.die}.w{r.worker % W}",
+                        "start", names[r.task]))
+            out.append((int(r.t_end), f"worker.x{r.die}.w{r.worker % W}",
+                        "complete", names[r.task]))
+    return out
