@@ -146,7 +146,7 @@ def build(args, device):
         from dataclasses import replace
         model = replace(model, num_layers=args.layers)
     g = build_decoder_layer(model, machine, graph_mode, args.batch,
-                            tile_overrides=device_tiles(model, machine, graph_mode),
+                            tile_overrides=device_tiles(model, machine, graph_mode, args.batch),
                             layers=model.num_layers)
     spec = Qwen3Spec.qwen3_8b(layers=model.num_layers)
     w = Qwen3Weights.random(spec, seed=0, device=f"cuda:{device}")

@@ -121,6 +121,7 @@ typedef struct mk_gemm_params {
   const void* res;    /* residual bf16 [M][ldres] or NULL                     */
   float* amax_val;    /* LOGITS: per-(worker,row) running max                 */
   int32_t* amax_idx;  /* LOGITS: per-(worker,row) argmax                      */
+  const void* norm_gamma; /* fused RMSNorm of x while staging (NULL = none)  */
   int32_t M, K, N;    /* N = weight rows of this task (N_local)               */
   int32_t T_M, T_N, T_K;
   int32_t ldx, ldy, ldres;
@@ -133,6 +134,8 @@ typedef struct mk_gemm_params {
   int32_t tile_n;
   int32_t amax_base;  /* LOGITS: first worker slot of this task             */
   int32_t amax_stride;/* LOGITS: rows per worker slot                       */
+  int32_t stage_x;    /* 1: stage x rows in shared memory per m-tile          */
+  float norm_eps;
 } mk_gemm_params;
 
 typedef struct mk_norm_params {
@@ -144,7 +147,7 @@ typedef struct mk_norm_params {
   void* x_store;       /* L0 only: gathered rows -> residual stream          */
   int32_t M, d;
   float eps;
-  int32_t pad;
+  int32_t fused;       /* 1: the consuming GEMM normalises; only gather here */
 } mk_norm_params;
 
 typedef struct mk_attn_params {
@@ -244,6 +247,8 @@ int64_t mk_log_read(mk_handle* h, mk_log_rec* out, int64_t max_records);
 int mk_tile_log_enable(mk_handle* h, int64_t capacity);
 int64_t mk_tile_log_read(mk_handle* h, int32_t* out4, int64_t max_records);
 int mk_set_watchdog(mk_handle* h, double seconds);
+/* Diagnostics only: bit0 = consumers skip GEMM math, bit1 = no TMA copies. */
+int mk_set_debug(mk_handle* h, int flags);
 int mk_destroy(mk_handle* h);
 const char* mk_last_error(void);
 int mk_version(void);

@@ -46,17 +46,18 @@ class Unit(C.Structure):
 
 class GemmParams(C.Structure):
     _fields_ = [("w", P), ("x", P), ("y", P), ("res", P), ("amax_val", P),
-                ("amax_idx", P), ("M", I32), ("K", I32), ("N", I32),
+                ("amax_idx", P), ("norm_gamma", P), ("M", I32), ("K", I32), ("N", I32),
                 ("T_M", I32), ("T_N", I32), ("T_K", I32), ("ldx", I32),
                 ("ldy", I32), ("ldres", I32), ("y_col0", I32),
                 ("epilogue", I32), ("traversal", I32), ("distribution", I32),
                 ("xcd", I32), ("tile_m", I32), ("tile_n", I32),
-                ("amax_base", I32), ("amax_stride", I32)]
+                ("amax_base", I32), ("amax_stride", I32), ("stage_x", I32),
+                ("norm_eps", F32)]
 
 
 class NormParams(C.Structure):
     _fields_ = [("x", P), ("gamma", P), ("y", P), ("embed", P), ("tokens", P),
-                ("x_store", P), ("M", I32), ("d", I32), ("eps", F32), ("pad", I32)]
+                ("x_store", P), ("M", I32), ("d", I32), ("eps", F32), ("fused", I32)]
 
 
 class AttnParams(C.Structure):
@@ -104,7 +105,7 @@ class LogRec(C.Structure):
 
 EXPORTS = ("mk_probe", "mk_probe_raw", "mk_create", "mk_step", "mk_sync", "mk_counters_get",
            "mk_counters_reset", "mk_log_enable", "mk_log_read",
-           "mk_tile_log_enable", "mk_tile_log_read", "mk_set_watchdog",
+           "mk_tile_log_enable", "mk_tile_log_read", "mk_set_watchdog", "mk_set_debug",
            "mk_destroy", "mk_last_error", "mk_version")
 
 _lib = None
@@ -134,6 +135,7 @@ def load() -> C.CDLL:
     lib.mk_tile_log_read.argtypes = [C.c_void_p, C.POINTER(I32), C.c_int64]
     lib.mk_tile_log_read.restype = C.c_int64
     lib.mk_set_watchdog.argtypes = [C.c_void_p, C.c_double]
+    lib.mk_set_debug.argtypes = [C.c_void_p, C.c_int]
     lib.mk_destroy.argtypes = [C.c_void_p]
     lib.mk_last_error.restype = C.c_char_p
     _lib = lib

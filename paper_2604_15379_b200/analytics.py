@@ -84,15 +84,20 @@ def fit_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
 
 
 def device_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
-                 t_m: int = 16, t_n: int = 8, max_t_k: int = 1024) -> dict:
-    """B200 tile overrides for the CUDA-core GEMM body.
+                 batch: int = 1, t_m: int = 16) -> dict:
+    """B200 tile overrides for the warp-row GEMM body (csrc gemm_tile).
 
-    One shared-memory ring slot holds ``R x T_K`` bf16 with ``R = T_N`` (or
-    ``2*T_N`` for the fused gate/up die task) and ``R*T_K <= 8192`` (16 KiB);
-    ``T_K`` is the largest power of two <= ``max_t_k`` dividing K, ``T_N``
-    the largest power of two <= ``t_n`` dividing the per-task width.  Passing
-    the result as ``tile_overrides`` to both builders keeps graph parity.
+    One shared-memory ring slot holds ``R x T_K`` bf16 (16 KiB) with
+    ``R = T_N`` rows (``2*T_N`` for the fused gate/up die task); each of the 8
+    consumer warps owns ``R/8`` rows.  More rows per warp amortise the
+    activation reads over more weights, so R grows with the batch rows per
+    m-tile: 8 rows for one row, 16 for up to 4, 32 beyond.  ``T_K`` is
+    ``8192 / R`` (or K itself when K < 256).  Passing the result as
+    ``tile_overrides`` to both builders keeps graph parity.
     """
+    rows = min(batch, t_m)
+    r_plain = 16 if rows <= 4 else 32
+    r_fused = 16 if rows <= 4 else 32
     out = {}
     for op in LINEAR_OPS:
         k, n = linear_gemm_dims(op, model)
@@ -100,14 +105,17 @@ def device_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
         width = n if graph_mode == "standard" else n // machine.num_xcds
         if fused:
             width //= 2
-        tk = max_t_k
+        r = r_fused if fused else r_plain
+        tn = r // 2 if fused else r
+        while width % tn and tn > (4 if fused else 8):
+            tn //= 2
+        r = 2 * tn if fused else tn
+        tk = min(8192 // r, k)
+        if k < 256:
+            tk = k
         while k % tk:
             tk //= 2
-        rows_cap = min(32 // (2 if fused else 1), 8192 // tk // (2 if fused else 1))
-        tn = min(t_n, rows_cap)
-        while width % tn:
-            tn //= 2
-        out[op] = (t_m, max(tn, 1), tk)
+        out[op] = (t_m, tn, tk)
     out["silu_chunk"] = min(STANDARD_TILE_PROFILE["silu_chunk"], model.ffn_dim)
     return out
 

@@ -49,7 +49,9 @@ constexpr int kConsWarps = 8;
 constexpr int kCons = kConsWarps * 32;          // consumer threads
 constexpr int kThreads = kCons + 32;            // + fetch warp
 constexpr int kSlotBytes = 16384;
-constexpr int kSlots = 12;
+constexpr int kSlots = 10;
+constexpr int kXsBytes = 32768;                 // staged activations per task
+constexpr int kMaxSplits = 128;                 // split-KV splits per row
 constexpr int kTQ = 32;                         // smem unit queue depth
 constexpr int kMailbox = 64;                    // mailbox depth per worker
 constexpr uint32_t kEnd = 0xFFFFFFu;
@@ -91,6 +93,14 @@ struct KArgs {
   int sched_mode;
   int W;
   uint32_t epoch;
+  int debug;               // bit0: consumers skip GEMM math, bit1: fetch issues no TMA
+};
+
+struct AttnScratch {
+  float vec[8][128];                // rotated q per head
+  float kn[128], vn[128];           // new token k / v
+  float st[8][288];                 // per-(warp,token-group) state; prologue scratch
+  float wsplit[8][kMaxSplits];      // reduce: per-(head, split) weights
 };
 
 struct Smem {
@@ -99,17 +109,18 @@ struct Smem {
   uint64_t tq_full[kTQ];
   uint64_t tq_empty[kTQ];
   int4 tq[kTQ];
-  float red[4][32][kMaxNB];         // GEMM cross-warp partial sums
-  float am_val[kAmaxRows];          // LM-head running max per row
-  int am_idx[kAmaxRows];
-  float vec[8][128];                // attention: rotated q per head
-  float kn[128], vn[128];           // attention: new token k / v
-  float st[8][288];                 // attention: per-(warp,token-group) state;
-                                    // also the prologue's pre-rope scratch
+  float amx_val[kConsWarps][kAmaxRows];   // LM head: per-warp running max per row
+  int amx_idx[kConsWarps][kAmaxRows];
   float bred[32];
   int ibred[32];
+  float rsum[kConsWarps][kMaxNB];   // x-staging: per-warp sums of squares
+  float rs[kMaxNB];                 // x-staging: 1/rms per staged row
   int4 cur;                         // consumer broadcast: current unit
   int abort_flag;
+  union __align__(16) {
+    AttnScratch at;
+    uint16_t xs[kXsBytes / 2];      // GEMM: staged (normalised) activations
+  } u;
 };
 
 // Scheduler CTAs never use the ring: their mailbox cursors live there.
@@ -210,8 +221,12 @@ __device__ bool fetch_slot(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   const int i = r.k % kSlots;
   const uint32_t round = r.k / kSlots;
   if (!mbar_wait(a, &s.empty[i], (round & 1) ^ 1, -2)) return false;
-  mbar_arrive_expect_tx(&s.full[i], bytes);
-  bulk_g2s(ring + size_t(i) * kSlotBytes, src, bytes, &s.full[i], pol);
+  if (a.debug & 2) {
+    mbar_arrive(&s.full[i]);
+  } else {
+    mbar_arrive_expect_tx(&s.full[i], bytes);
+    bulk_g2s(ring + size_t(i) * kSlotBytes, src, bytes, &s.full[i], pol);
+  }
   ++r.k;
   return true;
 }
@@ -269,23 +284,108 @@ __device__ __forceinline__ void cons_release_slot(Smem& s, Ring& r) {
 // GEMM tile body: y[m0:m0+rows, cols] = x[m0:.., :] . W_tile^T  (CUDA cores,
 // 128-bit weight streaming; weights come from the smem ring).
 // Slot layout: [R rows][T_K] bf16, thread ct owns 16-byte segments
-// ct, ct+256, ... -- all in one column (x reuse across rows).
+// ct, ct+256, ... -- all in one column (x reuse across rows).  Activations
+// come from the per-task staged copy in shared memory (XS) or, when the
+// rows do not fit, from global memory one slot ahead of use.
 // ---------------------------------------------------------------------------
-template <int NB>
+__device__ __forceinline__ void dot8_acc(const float (&w)[8], const float (&x)[8], float& acc) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc = fmaf(w[e], x[e], acc);
+}
+
+// Stage rows [m0, m0+rows) of x (K wide) into s.u.xs, optionally applying
+// Qwen3RMSNorm (fp32 statistics, cast, gamma) -- the rms task fused into its
+// consumer GEMM.  Bit-identical to run_rmsnorm's output.
+__device__ void stage_x(Smem& s, const mk_gemm_params& p, int m0, int rows, int ct) {
+  const uint16_t* x = reinterpret_cast<const uint16_t*>(p.x);
+  const int K = p.K;
+  const bool norm = p.norm_gamma != nullptr;
+  float ss[kMaxNB];
+#pragma unroll
+  for (int b = 0; b < kMaxNB; ++b) ss[b] = 0.f;
+#pragma unroll
+  for (int b = 0; b < kMaxNB; ++b) {
+    if (b < rows) {
+#pragma unroll 4
+      for (int k = ct * 8; k < K; k += kCons * 8) {
+        const uint4 v = ldg128_cg(x + size_t(m0 + b) * p.ldx + k);
+        *reinterpret_cast<uint4*>(&s.u.xs[b * K + k]) = v;
+        if (norm) {
+          float f[8];
+          unpack8(v, f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) ss[b] = fmaf(f[e], f[e], ss[b]);
+        }
+      }
+    }
+  }
+  if (norm) {
+    const int warp = ct >> 5, lane = ct & 31;
+#pragma unroll
+    for (int b = 0; b < kMaxNB; ++b) {
+      if (b < rows) {
+        float v = ss[b];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) s.rsum[warp][b] = v;
+      }
+    }
+    bar_sync(1, kCons);
+    if (ct < rows) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < kConsWarps; ++w) t += s.rsum[w][ct];
+      s.rs[ct] = rsqrtf(t / float(K) + p.norm_eps);
+    }
+    bar_sync(1, kCons);
+    const uint16_t* gam = reinterpret_cast<const uint16_t*>(p.norm_gamma);
+    for (int b = 0; b < rows; ++b) {
+      const float rs = s.rs[b];
+      for (int k = ct * 8; k < K; k += kCons * 8) {
+        float f[8], g[8];
+        unpack8(*reinterpret_cast<const uint4*>(&s.u.xs[b * K + k]), f);
+        unpack8(*reinterpret_cast<const uint4*>(gam + k), g);
+        uint16_t o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = f2bf(g[e] * bf2f(f2bf(f[e] * rs)));
+        *reinterpret_cast<uint4*>(&s.u.xs[b * K + k]) = *reinterpret_cast<uint4*>(o);
+      }
+    }
+  }
+  bar_sync(1, kCons);
+}
+
+// Warp-owned rows: slot [R rows][KC] bf16, warp w owns rows w, w+8, w+16,
+// w+24 (< R); lane l covers columns l*8 + 256*p of each row.  Partial dot
+// products stay in registers across the tile's K-chunks and are reduced
+// with warp shuffles only -- no CTA barrier per tile; each warp releases
+// ring slots on its own.  Fused gate/up: R = 2*T_N = 16, so warp w owns
+// gate row w and up row w+8 and applies SiLU itself.
+template <int NB, bool XS>
 __device__ void gemm_tile(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
                           const mk_gemm_params& p, int m, int n, int ct,
-                          int worker_slot) {
+                          float (&amv)[NB], int (&ami)[NB]) {
+  const int warp = ct >> 5, lane = ct & 31;
   const int R = gemm_rows(p);
+  const int rpw = R / kConsWarps;          // rows per warp (1, 2 or 4)
   const int KC = p.T_K;
-  const int spr = KC / 8;                 // segments per row (divides 256)
-  const int segs = R * spr;               // <= 1024
-  const int col8 = ct % spr;
-  const int rbase = ct / spr;
-  const int rstep = kCons / spr;
+  const int npass = KC >= 256 ? KC / 256 : 1;
+  const bool lane_on = lane * 8 < KC;      // KC < 256: upper lanes idle
   const int chunks = p.K / KC;
   const int m0 = m * p.T_M;
   const int rows_m = min(p.T_M, p.M - m0);
+  const int out_col0 = p.y_col0 + n * p.T_N;
+  const bool silu = p.epilogue == MK_EPI_SILU;
   const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(p.x);
+
+  // epilogue operands fetched before the stream: lane b holds row b
+  float resv[4] = {0.f, 0.f, 0.f, 0.f};
+  if (p.epilogue == MK_EPI_RESIDUAL && lane < rows_m) {
+    const uint16_t* res = reinterpret_cast<const uint16_t*>(p.res) + size_t(m0 + lane) * p.ldres;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j < rpw) resv[j] = bf2f(ldg16_cg(res + out_col0 + warp + kConsWarps * j));
+  }
 
   float acc[4][NB];
 #pragma unroll
@@ -295,54 +395,32 @@ __device__ void gemm_tile(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
 
   for (int c = 0; c < chunks; ++c) {
     cons_wait_slot(a, s, r);
-    const uint8_t* slot = ring + size_t(r.k % kSlots) * kSlotBytes;
-    const int kbase = c * KC + col8 * 8;
-    if constexpr (NB <= 8) {
-      float xf[NB][8];
+    if (!(a.debug & 1)) {
+      const uint8_t* slot = ring + size_t(r.k % kSlots) * kSlotBytes;
+      for (int ps = 0; ps < npass; ++ps) {
+        const int kin = ps * 256 + lane * 8;            // column inside the chunk
+        const int kg = c * KC + kin;                    // column in K
+        float wf[4][8];
 #pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        if (b < rows_m) {
-          uint4 v = ldg128_cg(x + size_t(m0 + b) * p.ldx + kbase);
-          unpack8(v, xf[b]);
-        } else {
+        for (int j = 0; j < 4; ++j) {
+          if (j < rpw && lane_on)
+            unpack8(lds128(slot + (size_t(warp + kConsWarps * j) * KC + kin) * 2), wf[j]);
+          else {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) xf[b][e] = 0.f;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int sg = ct + j * kCons;
-        if (sg < segs) {
-          float wf[8];
-          unpack8(lds128(slot + size_t(sg) * 16), wf);
-#pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            float t = acc[j][b];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) t = fmaf(wf[e], xf[b][e], t);
-            acc[j][b] = t;
+            for (int e = 0; e < 8; ++e) wf[j][e] = 0.f;
           }
         }
-      }
-    } else {
-      uint4 xr[NB];
 #pragma unroll
-      for (int b = 0; b < NB; ++b)
-        xr[b] = (b < rows_m) ? ldg128_cg(x + size_t(m0 + b) * p.ldx + kbase) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int sg = ct + j * kCons;
-        if (sg < segs) {
-          float wf[8];
-          unpack8(lds128(slot + size_t(sg) * 16), wf);
-#pragma unroll
-          for (int b = 0; b < NB; ++b) {
+        for (int b = 0; b < NB; ++b) {
+          if (b < rows_m && lane_on) {
+            uint4 xv;
+            if constexpr (XS) xv = *reinterpret_cast<const uint4*>(&s.u.xs[b * p.K + kg]);
+            else xv = ldg128_cg(x + size_t(m0 + b) * p.ldx + kg);
             float xf[8];
-            unpack8(xr[b], xf);
-            float t = acc[j][b];
+            unpack8(xv, xf);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) t = fmaf(wf[e], xf[e], t);
-            acc[j][b] = t;
+            for (int j = 0; j < 4; ++j)
+              if (j < rpw) dot8_acc(wf[j], xf, acc[j][b]);
           }
         }
       }
@@ -350,99 +428,225 @@ __device__ void gemm_tile(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
     cons_release_slot(s, r);
   }
 
-  // reduce the spr threads of each row: shuffles inside the warp, then smem
-  const int lanes = spr < 32 ? spr : 32;
+  // warp reduction: after the xor butterfly every lane holds every sum
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
+  for (int j = 0; j < 4; ++j) {
+    if (j >= rpw) continue;            // warp-uniform
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       float v = acc[j][b];
-      for (int off = lanes >> 1; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
       acc[j][b] = v;
     }
-  const int wsub = col8 / 32;
-  if ((col8 % lanes) == 0) {
+  }
+  // lane b writes batch row b (register-array reads use constant indices)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int sg = ct + j * kCons;
-      if (sg < segs) {
-        const int row = rbase + j * rstep;
+  for (int b = 0; b < NB; ++b) {
+    if (lane != b || b >= rows_m) continue;
+    if (p.epilogue == MK_EPI_LOGITS) {
+      float* y = reinterpret_cast<float*>(p.y);
 #pragma unroll
-        for (int b = 0; b < NB; ++b) s.red[wsub][row][b] = acc[j][b];
+      for (int j = 0; j < 4; ++j) {
+        if (j >= rpw) continue;
+        const int col = out_col0 + warp + kConsWarps * j;
+        const float v = acc[j][b];
+        if (y) y[size_t(m0 + b) * p.ldy + col] = v;
+        if (v > amv[b] || (v == amv[b] && col < ami[b])) { amv[b] = v; ami[b] = col; }
+      }
+    } else {
+      uint16_t* y = reinterpret_cast<uint16_t*>(p.y) + size_t(m0 + b) * p.ldy;
+      if (silu) {              // gate rows j < rpw/2, up rows j + rpw/2
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          if (j >= rpw / 2) continue;
+          const float g = acc[j][b], u = acc[j + rpw / 2 < 4 ? j + rpw / 2 : 3][b];
+          y[out_col0 + warp + kConsWarps * j] = f2bf(g / (1.f + __expf(-g)) * u);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j >= rpw) continue;
+          y[out_col0 + warp + kConsWarps * j] = f2bf(acc[j][b] + resv[j]);
+        }
       }
     }
   }
-  bar_sync(1, kCons);
-  const int nsub = (spr + 31) / 32;
-  const int out_rows = p.T_N;
-  const int out_col0 = p.y_col0 + n * p.T_N;
-  auto rowsum = [&](int row, int b) {
-    float v = 0.f;
-    for (int q = 0; q < nsub; ++q) v += s.red[q][row][b];
-    return v;
-  };
-  if (p.epilogue == MK_EPI_LOGITS) {
-    float* y = reinterpret_cast<float*>(p.y);
-    for (int e = ct; e < out_rows * rows_m; e += kCons) {
-      const int rr = e / rows_m, b = e % rows_m;
-      const float v = rowsum(rr, b);
-      if (y) y[size_t(m0 + b) * p.ldy + out_col0 + rr] = v;
-    }
-    if (ct < rows_m) {
-      const int b = m0 + ct;
-      float best = s.am_val[b];
-      int bi = s.am_idx[b];
-      for (int rr = 0; rr < out_rows; ++rr) {
-        const float v = rowsum(rr, ct);
-        const int col = out_col0 + rr;
-        if (v > best || (v == best && col < bi)) { best = v; bi = col; }
-      }
-      s.am_val[b] = best;
-      s.am_idx[b] = bi;
-    }
-  } else {
-    uint16_t* y = reinterpret_cast<uint16_t*>(p.y);
-    const uint16_t* res = reinterpret_cast<const uint16_t*>(p.res);
-    for (int e = ct; e < out_rows * rows_m; e += kCons) {
-      const int rr = e / rows_m, b = e % rows_m;
-      float v = rowsum(rr, b);
-      const size_t col = size_t(out_col0 + rr);
-      if (p.epilogue == MK_EPI_SILU) {
-        const float u = rowsum(rr + p.T_N, b);
-        v = v / (1.f + __expf(-v)) * u;
-      } else if (p.epilogue == MK_EPI_RESIDUAL) {
-        v += bf2f(ldg16_cg(res + size_t(m0 + b) * p.ldres + col));
-      }
-      y[size_t(m0 + b) * p.ldy + col] = f2bf(v);
-    }
-  }
-  bar_sync(1, kCons);   // red[] reused by the next tile
-  (void)worker_slot;
 }
 
-__device__ void run_gemm(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
-                         const mk_task& t, int worker, int gw, int tix, int ct,
-                         unsigned long long& tiles) {
-  const mk_gemm_params& p = *P<mk_gemm_params>(a, t);
-  const bool logits = p.epilogue == MK_EPI_LOGITS;
-  const int w_in_task = t.level == MK_LEVEL_CHIPLET ? worker : 0;
-  if (logits) {
-    for (int b = ct; b < p.M && b < kAmaxRows; b += kCons) {
-      s.am_val[b] = -INFINITY;
-      s.am_idx[b] = 0x7fffffff;
-    }
-    bar_sync(1, kCons);
+// Fast path: rows per warp RPW in {1,2,4}, K-chunk KC = 1024/RPW (so one
+// slot = 8*RPW rows x KC = 16 KiB and every lane covers NP = 4/RPW 16-byte
+// segments per row).  All slot loads are issued before any math, the slot is
+// released as soon as the weights sit in registers, and independent
+// accumulator chains keep the FMA pipe busy.
+template <int NB, int RPW, bool XS>
+__device__ void gemm_tile_fast(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
+                               const mk_gemm_params& p, int m, int n, int ct,
+                               float (&amv)[NB], int (&ami)[NB]) {
+  constexpr int NP = 4 / RPW;
+  constexpr int KC = 256 * NP;
+  constexpr int CH = (RPW * NB >= 4) ? 1 : NP;   // extra chains when few (row, b) pairs
+  const int warp = ct >> 5, lane = ct & 31;
+  const int chunks = p.K / KC;
+  const int m0 = m * p.T_M;
+  const int rows_m = min(p.T_M, p.M - m0);
+  const int out_col0 = p.y_col0 + n * p.T_N;
+  const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(p.x);
+
+  float resv[RPW];
+#pragma unroll
+  for (int j = 0; j < RPW; ++j) resv[j] = 0.f;
+  if (p.epilogue == MK_EPI_RESIDUAL && lane < rows_m) {
+    const uint16_t* res = reinterpret_cast<const uint16_t*>(p.res) + size_t(m0 + lane) * p.ldres;
+#pragma unroll
+    for (int j = 0; j < RPW; ++j) resv[j] = bf2f(ldg16_cg(res + out_col0 + warp + kConsWarps * j));
   }
+
+  float acc[CH][RPW][NB];
+#pragma unroll
+  for (int q = 0; q < CH; ++q)
+#pragma unroll
+    for (int j = 0; j < RPW; ++j)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) acc[q][j][b] = 0.f;
+
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t xs_s = smem_u32(s.u.xs);
+  for (int c = 0; c < chunks; ++c) {
+    cons_wait_slot(a, s, r);
+    const uint32_t slot = ring_s + uint32_t(r.k % kSlots) * kSlotBytes;
+    uint4 wv[NP][RPW];
+#pragma unroll
+    for (int ps = 0; ps < NP; ++ps)
+#pragma unroll
+      for (int j = 0; j < RPW; ++j)
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(wv[ps][j].x), "=r"(wv[ps][j].y), "=r"(wv[ps][j].z), "=r"(wv[ps][j].w)
+                     : "r"(slot + uint32_t(((warp + kConsWarps * j) * KC + ps * 256 + lane * 8) * 2)));
+    uint4 xv[NP][NB];
+#pragma unroll
+    for (int ps = 0; ps < NP; ++ps)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int kg = c * KC + ps * 256 + lane * 8;
+        if constexpr (XS) {
+          if (b < rows_m)
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(xv[ps][b].x), "=r"(xv[ps][b].y), "=r"(xv[ps][b].z), "=r"(xv[ps][b].w)
+                         : "r"(xs_s + uint32_t((b * p.K + kg) * 2)));
+          else xv[ps][b] = make_uint4(0, 0, 0, 0);
+        } else {
+          xv[ps][b] = (b < rows_m) ? ldg128_cg(x + size_t(m0 + b) * p.ldx + kg) : make_uint4(0, 0, 0, 0);
+        }
+      }
+    cons_release_slot(s, r);          // weights now live in registers
+    if (a.debug & 1) continue;
+#pragma unroll
+    for (int ps = 0; ps < NP; ++ps) {
+      float wf[RPW][8];
+#pragma unroll
+      for (int j = 0; j < RPW; ++j) unpack8(wv[ps][j], wf[j]);
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        float xf[8];
+        unpack8(xv[ps][b], xf);
+#pragma unroll
+        for (int j = 0; j < RPW; ++j) {
+          float& t = acc[CH == 1 ? 0 : ps][j][b];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) t = fmaf(wf[j][e], xf[e], t);
+        }
+      }
+    }
+  }
+
+  float tot[RPW][NB];
+#pragma unroll
+  for (int j = 0; j < RPW; ++j)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      float v = acc[0][j][b];
+#pragma unroll
+      for (int q = 1; q < CH; ++q) v += acc[q][j][b];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      tot[j][b] = v;
+    }
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    if (lane != b || b >= rows_m) continue;
+    if (p.epilogue == MK_EPI_LOGITS) {
+      float* y = reinterpret_cast<float*>(p.y);
+#pragma unroll
+      for (int j = 0; j < RPW; ++j) {
+        const int col = out_col0 + warp + kConsWarps * j;
+        const float v = tot[j][b];
+        if (y) y[size_t(m0 + b) * p.ldy + col] = v;
+        if (v > amv[b] || (v == amv[b] && col < ami[b])) { amv[b] = v; ami[b] = col; }
+      }
+    } else {
+      uint16_t* y = reinterpret_cast<uint16_t*>(p.y) + size_t(m0 + b) * p.ldy;
+      if (p.epilogue == MK_EPI_SILU) {
+        if constexpr (RPW >= 2) {
+#pragma unroll
+          for (int j = 0; j < RPW / 2; ++j) {
+            const float g = tot[j][b], u = tot[j + RPW / 2][b];
+            y[out_col0 + warp + kConsWarps * j] = f2bf(g / (1.f + __expf(-g)) * u);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < RPW; ++j) y[out_col0 + warp + kConsWarps * j] = f2bf(tot[j][b] + resv[j]);
+      }
+    }
+  }
+}
+
+template <int NB, bool XS>
+__device__ void gemm_task(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
+                          const mk_gemm_params& p, int w_in_task, int gw, int tix, int ct,
+                          unsigned long long& tiles) {
+  const int warp = ct >> 5, lane = ct & 31;
+  float amv[NB];
+  int ami[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) { amv[b] = -INFINITY; ami[b] = 0x7fffffff; }
   TileIter it;
   it.init(p, a.W, w_in_task);
-  int m, n;
+  int m, n, staged_m = -1;
+  int cur_m = -1;
   while (it.next(m, n)) {
-    const int rows_m = min(p.T_M, p.M - m * p.T_M);
-    if (rows_m <= 1) gemm_tile<1>(a, s, ring, r, p, m, n, ct, w_in_task);
-    else if (rows_m <= 2) gemm_tile<2>(a, s, ring, r, p, m, n, ct, w_in_task);
-    else if (rows_m <= 4) gemm_tile<4>(a, s, ring, r, p, m, n, ct, w_in_task);
-    else if (rows_m <= 8) gemm_tile<8>(a, s, ring, r, p, m, n, ct, w_in_task);
-    else gemm_tile<16>(a, s, ring, r, p, m, n, ct, w_in_task);
+    if (p.epilogue == MK_EPI_LOGITS && m != cur_m) {
+      // switch the lanes' running argmax to the rows of the new m-tile
+      // (lane b always owns row m0 + b, so no cross-lane hazard)
+      const int mo = cur_m * p.T_M, mn = m * p.T_M;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        if (lane != b) continue;
+        if (cur_m >= 0 && mo + b < p.M) { s.amx_val[warp][mo + b] = amv[b]; s.amx_idx[warp][mo + b] = ami[b]; }
+        if (mn + b < p.M) { amv[b] = s.amx_val[warp][mn + b]; ami[b] = s.amx_idx[warp][mn + b]; }
+      }
+    }
+    cur_m = m;
+    if constexpr (XS) {
+      if (m != staged_m) {
+        stage_x(s, p, m * p.T_M, min(p.T_M, p.M - m * p.T_M), ct);
+        staged_m = m;
+      }
+    }
+    // fast path for the register-feasible (rows-per-warp, batch) pairs
+    const int R = gemm_rows(p);
+    bool done = false;
+    if constexpr (NB == 1) {
+      if (R == 8 && p.T_K == 1024) { gemm_tile_fast<NB, 1, XS>(a, s, ring, r, p, m, n, ct, amv, ami); done = true; }
+    }
+    if constexpr (NB <= 4) {
+      if (!done && R == 16 && p.T_K == 512) { gemm_tile_fast<NB, 2, XS>(a, s, ring, r, p, m, n, ct, amv, ami); done = true; }
+    }
+    if constexpr (NB <= 8) {
+      if (!done && R == 32 && p.T_K == 256) { gemm_tile_fast<NB, 4, XS>(a, s, ring, r, p, m, n, ct, amv, ami); done = true; }
+    }
+    if (!done) gemm_tile<NB, XS>(a, s, ring, r, p, m, n, ct, amv, ami);
     if (ct == 0) {
       ++tiles;
       if (a.tile_log) {
@@ -454,18 +658,57 @@ __device__ void run_gemm(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
       }
     }
   }
-  if (logits) {
+  if (p.epilogue == MK_EPI_LOGITS) {
+    if (cur_m >= 0) {
+      const int m0 = cur_m * p.T_M;
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        if (lane == b && m0 + b < p.M) { s.amx_val[warp][m0 + b] = amv[b]; s.amx_idx[warp][m0 + b] = ami[b]; }
+    }
+    bar_sync(1, kCons);
     const int slot = p.amax_base + w_in_task;
     for (int b = ct; b < p.M && b < kAmaxRows; b += kCons) {
-      p.amax_val[size_t(slot) * p.amax_stride + b] = s.am_val[b];
-      p.amax_idx[size_t(slot) * p.amax_stride + b] = s.am_idx[b];
+      float best = -INFINITY;
+      int bi = 0x7fffffff;
+      for (int w = 0; w < kConsWarps; ++w) {
+        const float v = s.amx_val[w][b];
+        const int i = s.amx_idx[w][b];
+        if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+      }
+      p.amax_val[size_t(slot) * p.amax_stride + b] = best;
+      p.amax_idx[size_t(slot) * p.amax_stride + b] = bi;
     }
   }
+  bar_sync(1, kCons);   // staged rows / amx[] reusable by the next unit
+}
+
+__device__ void run_gemm(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
+                         const mk_task& t, int worker, int gw, int tix, int ct,
+                         unsigned long long& tiles) {
+  const mk_gemm_params& p = *P<mk_gemm_params>(a, t);
+  const int w_in_task = t.level == MK_LEVEL_CHIPLET ? worker : 0;
+  if (p.epilogue == MK_EPI_LOGITS) {
+    for (int e = ct; e < kConsWarps * kAmaxRows; e += kCons) {
+      s.amx_val[e / kAmaxRows][e % kAmaxRows] = -INFINITY;
+      s.amx_idx[e / kAmaxRows][e % kAmaxRows] = 0x7fffffff;
+    }
+    bar_sync(1, kCons);
+  }
+  const int rows = min(p.T_M, p.M);
+#define MK_GEMM_NB(XSV)                                                              \
+  if (rows <= 1) gemm_task<1, XSV>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles); \
+  else if (rows <= 2) gemm_task<2, XSV>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles); \
+  else if (rows <= 4) gemm_task<4, XSV>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles); \
+  else if (rows <= 8) gemm_task<8, XSV>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles); \
+  else gemm_task<16, XSV>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles);
+  if (p.stage_x) { MK_GEMM_NB(true) } else { MK_GEMM_NB(false) }
+#undef MK_GEMM_NB
 }
 
 // ---------------------------------------------------------------------------
 // RMSNorm (Qwen3RMSNorm: fp32 statistics, cast, gamma multiply), optional
-// embedding gather for layer 0.
+// embedding gather for layer 0.  When the lowering fused the norm into the
+// consuming GEMM (mk_norm_params.fused), only the gather remains.
 // ---------------------------------------------------------------------------
 __device__ float block_sum(Smem& s, float v, int ct) {
 #pragma unroll
@@ -486,6 +729,13 @@ __device__ void run_rmsnorm(const KArgs& a, Smem& s, const mk_task& t, int ib, i
     const uint16_t* src;
     if (p.embed) src = reinterpret_cast<const uint16_t*>(p.embed) + size_t(p.tokens[b]) * p.d;
     else src = reinterpret_cast<const uint16_t*>(p.x) + size_t(b) * p.d;
+    uint16_t* xs = p.x_store ? reinterpret_cast<uint16_t*>(p.x_store) + size_t(b) * p.d : nullptr;
+    if (p.fused) {            // consumer GEMM normalises; keep only the gather
+      if (xs)
+        for (int k = ct * 8; k < p.d; k += kCons * 8)
+          *reinterpret_cast<uint4*>(xs + k) = ldg128_cg(src + k);
+      continue;
+    }
     float ss = 0.f;
     for (int k = ct * 8; k < p.d; k += kCons * 8) {
       float f[8];
@@ -496,7 +746,6 @@ __device__ void run_rmsnorm(const KArgs& a, Smem& s, const mk_task& t, int ib, i
     const float tot = block_sum(s, ss, ct);
     const float rs = rsqrtf(tot / float(p.d) + p.eps);
     uint16_t* y = reinterpret_cast<uint16_t*>(p.y) + size_t(b) * p.d;
-    uint16_t* xs = p.x_store ? reinterpret_cast<uint16_t*>(p.x_store) + size_t(b) * p.d : nullptr;
     for (int k = ct * 8; k < p.d; k += kCons * 8) {
       const uint4 raw = ldg128_cg(src + k);
       float f[8], g[8];
@@ -518,25 +767,27 @@ __device__ void run_rmsnorm(const KArgs& a, Smem& s, const mk_task& t, int ib, i
 // Attention partial: QK-norm + RoPE (+ KV append for the new token) and a
 // split-KV online-softmax partial over cached tokens streamed into the ring.
 // ---------------------------------------------------------------------------
+// One warp: per-head RMSNorm over HD (vector loads), cast, gamma, RoPE.
 template <int HD>
-__device__ void head_norm_rope(Smem& s, const uint16_t* src, const uint16_t* gam, float eps,
+__device__ void head_norm_rope(const uint16_t* src, const uint16_t* gam, float eps,
                                const float* cs, const float* sn, float* out, int lane,
                                float* scratch) {
-  float v[(HD + 31) / 32];
+  constexpr int LN = HD / 8;            // lanes holding 8 elements each
+  const bool act = lane < LN;
+  const uint4 fv = act ? ldg128_cg(src + lane * 8) : make_uint4(0, 0, 0, 0);
+  const uint4 gv = act ? *reinterpret_cast<const uint4*>(gam + lane * 8) : make_uint4(0, 0, 0, 0);
+  float f[8], g[8];
+  unpack8(fv, f);
+  unpack8(gv, g);
   float ss = 0.f;
 #pragma unroll
-  for (int k = 0; k < (HD + 31) / 32; ++k) {
-    const int d = lane + 32 * k;
-    v[k] = d < HD ? bf2f(ldg16_cg(src + d)) : 0.f;
-    ss = fmaf(v[k], v[k], ss);
-  }
+  for (int e = 0; e < 8; ++e) ss = fmaf(f[e], f[e], ss);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
   const float rs = rsqrtf(ss / float(HD) + eps);
+  if (lane < LN) {
 #pragma unroll
-  for (int k = 0; k < (HD + 31) / 32; ++k) {
-    const int d = lane + 32 * k;
-    if (d < HD) scratch[d] = bf2f(gam[d]) * bf2f(f2bf(v[k] * rs));
+    for (int e = 0; e < 8; ++e) scratch[lane * 8 + e] = g[e] * bf2f(f2bf(f[e] * rs));
   }
   __syncwarp();
   constexpr int H2 = HD / 2;
@@ -547,12 +798,12 @@ __device__ void head_norm_rope(Smem& s, const uint16_t* src, const uint16_t* gam
     out[i + H2] = x2 * c + x1 * sv;
   }
   __syncwarp();
-  (void)s;
 }
 
 template <int HD>
 __device__ void attn_item(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
-                          const mk_attn_params& p, int item, int ct) {
+                          const mk_attn_params& p, int item, int ct, int& q_row) {
+  AttnScratch& at = s.u.at;
   const int b = item / p.n_splits, sp = item % p.n_splits;
   const int pos = p.positions[b];
   const int t0 = sp * p.split;
@@ -565,11 +816,13 @@ __device__ void attn_item(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   const float* cs = p.rope_cos + size_t(pos) * (HD / 2);
   const float* sn = p.rope_sin + size_t(pos) * (HD / 2);
 
-  // prologue: q heads of this group (warps 0..G-1), new k (warp G%8 after)
-  if (warp < G) {
+  // prologue (once per batch row within a unit): q heads of this group
+  // (warps 0..G-1); the new token's k/v by warp G (or after a barrier)
+  const bool need_q = q_row != b;
+  if (need_q && warp < G) {
     const int qh = p.kv_head * G + warp;
-    head_norm_rope<HD>(s, qkv + qh * HD, reinterpret_cast<const uint16_t*>(p.q_gamma), p.eps,
-                       cs, sn, s.vec[warp], lane, s.st[warp]);
+    head_norm_rope<HD>(qkv + qh * HD, reinterpret_cast<const uint16_t*>(p.q_gamma), p.eps,
+                       cs, sn, at.vec[warp], lane, at.st[warp]);
   }
   if (has_new) {
     const int kw = G < kConsWarps ? G : 0;
@@ -577,21 +830,22 @@ __device__ void attn_item(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
     if (warp == kw) {
       const int koff = p.q_heads * HD + p.kv_head * HD;
       const int voff = (p.q_heads + p.kv_heads) * HD + p.kv_head * HD;
-      head_norm_rope<HD>(s, qkv + koff, reinterpret_cast<const uint16_t*>(p.k_gamma), p.eps,
-                         cs, sn, s.kn, lane, s.st[kw]);
+      head_norm_rope<HD>(qkv + koff, reinterpret_cast<const uint16_t*>(p.k_gamma), p.eps,
+                         cs, sn, at.kn, lane, at.st[kw]);
       const size_t crow = ((size_t(b) * p.kv_heads + p.kv_head) * p.t_max + pos) * HD;
       uint16_t* kc = reinterpret_cast<uint16_t*>(p.k_cache) + crow;
       uint16_t* vc = reinterpret_cast<uint16_t*>(p.v_cache) + crow;
       for (int d = lane; d < HD; d += 32) {
         const uint16_t vv = ldg16_cg(qkv + voff + d);
-        const uint16_t kb = f2bf(s.kn[d]);
-        s.vn[d] = bf2f(vv);
+        const uint16_t kb = f2bf(at.kn[d]);
+        at.vn[d] = bf2f(vv);
         kc[d] = kb;
         vc[d] = vv;
-        s.kn[d] = bf2f(kb);      // attend to the rounded (cached) key, as later steps will
+        at.kn[d] = bf2f(kb);     // attend to the rounded (cached) key, as later steps will
       }
     }
   }
+  q_row = b;
   bar_sync(1, kCons);
 
   constexpr int LPT = HD / 8;          // lanes per token
@@ -601,7 +855,7 @@ __device__ void attn_item(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   const float qscale = p.scale * 1.4426950408889634f;
   float q8[8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) q8[e] = s.vec[head][dl * 8 + e] * qscale;
+  for (int e = 0; e < 8; ++e) q8[e] = at.vec[head][dl * 8 + e] * qscale;
 
   const uint8_t* kslot = nullptr;
   const uint8_t* vslot = nullptr;
@@ -626,8 +880,8 @@ __device__ void attn_item(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
     } else {
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        kf[e] = valid ? s.kn[dl * 8 + e] : 0.f;
-        vf[e] = valid ? s.vn[dl * 8 + e] : 0.f;
+        kf[e] = valid ? at.kn[dl * 8 + e] : 0.f;
+        vf[e] = valid ? at.vn[dl * 8 + e] : 0.f;
       }
     }
     float sc = 0.f;
@@ -650,8 +904,8 @@ __device__ void attn_item(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
     cons_release_slot(s, r);
   }
   // combine the (warp, token-group) states of each head
-  bar_sync(1, kCons);            // prologue scratch (s.st) no longer read
-  float* st = s.st[warp] + tg * (HD + 2);
+  bar_sync(1, kCons);            // prologue scratch (st) no longer read
+  float* st = at.st[warp] + tg * (HD + 2);
 #pragma unroll
   for (int e = 0; e < 8; ++e) st[dl * 8 + e] = o[e];
   if (dl == 0) { st[HD] = mx; st[HD + 1] = l; }
@@ -661,11 +915,11 @@ __device__ void attn_item(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
     const int hh = e / HD, d = e % HD;
     float M = -INFINITY;
     for (int q = 0; q < nsub; ++q)
-      for (int g2 = 0; g2 < TPI; ++g2) M = fmaxf(M, s.st[q * G + hh][g2 * (HD + 2) + HD]);
+      for (int g2 = 0; g2 < TPI; ++g2) M = fmaxf(M, at.st[q * G + hh][g2 * (HD + 2) + HD]);
     float acc = 0.f, den = 0.f;
     for (int q = 0; q < nsub; ++q)
       for (int g2 = 0; g2 < TPI; ++g2) {
-        const float* x = s.st[q * G + hh] + g2 * (HD + 2);
+        const float* x = at.st[q * G + hh] + g2 * (HD + 2);
         if (x[HD] == -INFINITY) continue;
         const float f = exp2f(x[HD] - M);
         acc = fmaf(f, x[d], acc);
@@ -681,38 +935,66 @@ __device__ void attn_item(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
 __device__ void run_attn_partial(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
                                  const mk_task& t, int ib, int ie, int ct) {
   const mk_attn_params& p = *P<mk_attn_params>(a, t);
+  int q_row = -1;
   for (int i = ib; i < ie; ++i) {
     switch (p.head_dim) {
-      case 128: attn_item<128>(a, s, ring, r, p, i, ct); break;
-      case 64: attn_item<64>(a, s, ring, r, p, i, ct); break;
-      case 32: attn_item<32>(a, s, ring, r, p, i, ct); break;
-      default: attn_item<16>(a, s, ring, r, p, i, ct); break;
+      case 128: attn_item<128>(a, s, ring, r, p, i, ct, q_row); break;
+      case 64: attn_item<64>(a, s, ring, r, p, i, ct, q_row); break;
+      case 32: attn_item<32>(a, s, ring, r, p, i, ct, q_row); break;
+      default: attn_item<16>(a, s, ring, r, p, i, ct, q_row); break;
     }
   }
 }
 
-__device__ void run_attn_reduce(const KArgs& a, const mk_task& t, int ib, int ie, int ct) {
+// Merge the split partials of one kv head for rows [ib, ie): all (head, split)
+// maxima load in parallel, then every (head, dim) thread streams its splits.
+__device__ void run_attn_reduce(const KArgs& a, Smem& s, const mk_task& t, int ib, int ie, int ct) {
   const mk_attn_params& p = *P<mk_attn_params>(a, t);
+  AttnScratch& at = s.u.at;
   const int HD = p.head_dim, G = p.group;
   uint16_t* out = reinterpret_cast<uint16_t*>(p.out);
   for (int b = ib; b < ie; ++b) {
     const int pos = p.positions[b];
-    const int nv = pos / p.split + 1;
+    const int nv = min(pos / p.split + 1, kMaxSplits);
     const float* base = p.partial + (size_t(b) * p.kv_heads + p.kv_head) * p.n_splits * G * (HD + 4);
+    // weights: w[h][s] = exp2(m_s - M_h) for every split; the denominator
+    // sum_s w*l goes into slot kMaxSplits-1's neighbour via a second pass
+    for (int e = ct; e < G * nv; e += kCons) {
+      const int hh = e / nv, sp = e % nv;
+      at.wsplit[hh][sp] = __ldcg(base + (size_t(sp) * G + hh) * (HD + 4) + HD);
+    }
+    bar_sync(1, kCons);
+    if (ct < G) {
+      float M = -INFINITY;
+      for (int sp = 0; sp < nv; ++sp) M = fmaxf(M, at.wsplit[ct][sp]);
+      float den = 0.f;
+      for (int sp = 0; sp < nv; ++sp) {
+        const float w = exp2f(at.wsplit[ct][sp] - M);
+        den = fmaf(w, __ldcg(base + (size_t(sp) * G + ct) * (HD + 4) + HD + 1), den);
+        at.wsplit[ct][sp] = w;
+      }
+      s.bred[ct] = 1.f / den;
+    }
+    bar_sync(1, kCons);
     for (int e = ct; e < G * HD; e += kCons) {
       const int hh = e / HD, d = e % HD;
-      float M = -INFINITY;
-      for (int sp = 0; sp < nv; ++sp)
-        M = fmaxf(M, __ldcg(base + (size_t(sp) * G + hh) * (HD + 4) + HD));
-      float num = 0.f, den = 0.f;
-      for (int sp = 0; sp < nv; ++sp) {
-        const float* x = base + (size_t(sp) * G + hh) * (HD + 4);
-        const float f = exp2f(__ldcg(x + HD) - M);
-        num = fmaf(f, __ldcg(x + d), num);
-        den = fmaf(f, __ldcg(x + HD + 1), den);
+      const float* col = base + size_t(hh) * (HD + 4) + d;
+      float num = 0.f;
+      int sp = 0;
+      for (; sp + 4 <= nv; sp += 4) {
+        const float o0 = __ldcg(col + size_t(sp) * G * (HD + 4));
+        const float o1 = __ldcg(col + size_t(sp + 1) * G * (HD + 4));
+        const float o2 = __ldcg(col + size_t(sp + 2) * G * (HD + 4));
+        const float o3 = __ldcg(col + size_t(sp + 3) * G * (HD + 4));
+        num = fmaf(at.wsplit[hh][sp], o0, num);
+        num = fmaf(at.wsplit[hh][sp + 1], o1, num);
+        num = fmaf(at.wsplit[hh][sp + 2], o2, num);
+        num = fmaf(at.wsplit[hh][sp + 3], o3, num);
       }
-      out[size_t(b) * p.q_heads * HD + (p.kv_head * G + hh) * HD + d] = f2bf(num / den);
+      for (; sp < nv; ++sp) num = fmaf(at.wsplit[hh][sp], __ldcg(col + size_t(sp) * G * (HD + 4)), num);
+      out[size_t(b) * p.q_heads * HD + (p.kv_head * G + hh) * HD + d] = f2bf(num * s.bred[hh]);
     }
+    bar_sync(1, kCons);
   }
 }
 
@@ -924,7 +1206,7 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
       case MK_OP_GEMM: run_gemm(a, s, ring, r, t, worker, gw, ent.x, ct, n_tiles); break;
       case MK_OP_RMSNORM: run_rmsnorm(a, s, t, ent.y, ent.z, ct); break;
       case MK_OP_ATTN_PARTIAL: run_attn_partial(a, s, ring, r, t, ent.y, ent.z, ct); break;
-      case MK_OP_ATTN_REDUCE: run_attn_reduce(a, t, ent.y, ent.z, ct); break;
+      case MK_OP_ATTN_REDUCE: run_attn_reduce(a, s, t, ent.y, ent.z, ct); break;
       case MK_OP_SILU: run_silu(a, t, ct); break;
       case MK_OP_ARGMAX: run_argmax(a, s, t, ent.y, ent.z, ct); break;
       default: break;
@@ -1065,6 +1347,7 @@ struct mk_handle {
   int n_events = 0, n_tasks = 0, n_units = 0, n_sub = 0;
   uint32_t epoch = 0;
   double watchdog_s = 5.0;
+  int debug = 0;
   // device buffers
   mk_task* d_tasks = nullptr;
   mk_unit* d_units = nullptr;
@@ -1260,9 +1543,13 @@ static int validate_graph(const mk_graph_desc* g) {
       const mk_gemm_params* p = reinterpret_cast<const mk_gemm_params*>(
           static_cast<const uint8_t*>(g->params) + t.param_off);
       const int R = p->T_N * (p->epilogue == MK_EPI_SILU ? 2 : 1);
-      const int spr = p->T_K / 8;
-      if (p->T_K % 8 || p->T_K > 1024 || 256 % spr || p->K % p->T_K || size_t(R) * p->T_K * 2 > size_t(kSlotBytes) ||
-          p->N % R || p->T_M > kMaxNB || R > 32 || (p->epilogue == MK_EPI_LOGITS && p->M > kAmaxRows))
+      const bool kc_ok = (p->T_K % 256 == 0) || (p->T_K == p->K && p->T_K % 8 == 0 && p->T_K < 256);
+      if (!kc_ok || p->K % p->T_K || size_t(R) * p->T_K * 2 > size_t(kSlotBytes) ||
+          R % kConsWarps || R > 4 * kConsWarps ||
+          (p->epilogue == MK_EPI_SILU && (R / kConsWarps) % 2) ||
+          p->N % R || p->T_M > kMaxNB || (p->epilogue == MK_EPI_LOGITS && p->M > kAmaxRows) ||
+          (p->stage_x && size_t(std::min(p->T_M, p->M)) * p->K * 2 > size_t(kXsBytes)) ||
+          (p->norm_gamma && !p->stage_x))
         return fail(MK_ERR_CONFIG, "gemm task " + std::to_string(i) + " has an unsupported tile (" +
                                        std::to_string(p->T_M) + "," + std::to_string(p->T_N) + "," +
                                        std::to_string(p->T_K) + ")");
@@ -1272,7 +1559,7 @@ static int validate_graph(const mk_graph_desc* g) {
           static_cast<const uint8_t*>(g->params) + t.param_off);
       const int hd = p->head_dim;
       if ((hd != 16 && hd != 32 && hd != 64 && hd != 128) || p->group < 1 || p->group > 8 ||
-          8 % p->group || size_t(p->split) * hd * 2 > size_t(kSlotBytes))
+          8 % p->group || size_t(p->split) * hd * 2 > size_t(kSlotBytes) || p->n_splits > kMaxSplits)
         return fail(MK_ERR_CONFIG, "attention task " + std::to_string(i) + " has unsupported shapes");
     }
   }
@@ -1401,6 +1688,7 @@ int mk_step(mk_handle* h, void* stream) {
   a.watchdog_ns = (unsigned long long)(h->watchdog_s * 1e9);
   a.n_events = h->n_events; a.n_sched = h->n_sched; a.sched_mode = h->sched_mode; a.W = h->W;
   a.epoch = h->epoch;
+  a.debug = h->debug;
   void* args[] = {&a};
   CK(cudaLaunchCooperativeKernel((const void*)megakernel, dim3(h->num_sms), dim3(kThreads), args,
                                  kSmemBytes, static_cast<cudaStream_t>(stream)));
@@ -1490,6 +1778,12 @@ int64_t mk_tile_log_read(mk_handle* h, int32_t* out4, int64_t max_records) {
 int mk_set_watchdog(mk_handle* h, double seconds) {
   if (!h || !(seconds > 0)) return fail(MK_ERR_CONFIG, "bad watchdog");
   h->watchdog_s = seconds;
+  return MK_OK;
+}
+
+int mk_set_debug(mk_handle* h, int flags) {
+  if (!h) return fail(MK_ERR_CONFIG, "null handle");
+  h->debug = flags;
   return MK_OK;
 }
 

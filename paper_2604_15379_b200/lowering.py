@@ -48,6 +48,10 @@ class LoweringOptions:
     fanout: bool = True            # split CU tasks' items over several units
     lm_tile: tuple = (16, 8, 1024)  # (T_M, T_N, T_K) of the appended LM head
     attn_split: int = 64           # tokens per split-KV item
+    fuse_norm: bool = True         # RMSNorm folded into the consuming GEMM's
+                                   # activation staging when the rows fit
+
+XS_BYTES = 32768                   # kXsBytes in mk_kernel.cu
 
 
 @dataclass
@@ -160,9 +164,17 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                 units_by_sched[s].append((ti, ib, ie))
         return ti
 
+    def stages(M, K, tile):
+        return min(tile[0], M) * K * 2 <= XS_BYTES
+
     def gemm_params(w, x, y, res, M, K, N, tile, ldx, ldy, ldres, col0, epi,
-                    xcd, tm=-1, tn=-1, amax_base=0):
+                    xcd, tm=-1, tn=-1, amax_base=0, gamma=None):
         p = L.GemmParams()
+        p.stage_x = 1 if stages(M, K, tile) else 0
+        if gamma is not None:
+            assert p.stage_x
+            p.norm_gamma = _ptr(gamma)
+            p.norm_eps = spec.eps
         p.w, p.x, p.y, p.res = w, x, y, res
         p.amax_val = _ptr(bufs.amax_val)
         p.amax_idx = _ptr(bufs.amax_idx)
@@ -174,8 +186,9 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         p.amax_base, p.amax_stride = amax_base, B
         return blob.add(p)
 
-    def norm_params(layer_bufs, x, gamma, y, embed=False):
+    def norm_params(layer_bufs, x, gamma, y, embed=False, fused=False):
         p = L.NormParams()
+        p.fused = 1 if fused else 0
         p.x, p.gamma, p.y = _ptr(x), _ptr(gamma), _ptr(y)
         if embed:
             p.embed = _ptr(bufs.embed)
@@ -202,6 +215,16 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         p.eps, p.scale = spec.eps, hd ** -0.5
         return blob.add(p)
 
+    def gemm_tile_of(kind):
+        for t in g.tasks:
+            if t.op_kind is kind:
+                return tuple(t.tile_shape)
+        return None
+
+    fuse = opts.fuse_norm and all(
+        stages(B, d, tl) for tl in (gemm_tile_of(OpKind.QKV_PROJ),
+                                    gemm_tile_of(OpKind.GATE_UP_SILU),
+                                    opts.lm_tile))
     u_attn = _cdiv(total_workers, spec.kv_heads)
     u_rows = min(B, 16)
     silu_meta = _silu_meta(g, B, F)
@@ -219,9 +242,10 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
             if first:
                 src = bufs.x_in0 if layer == 0 else bufs.layers[layer - 1]["x_out"]
                 po = norm_params(lb, src, wl["in_norm"], lb["normed1"],
-                                 embed=(layer == 0))
+                                 embed=(layer == 0), fused=fuse)
             else:
-                po = norm_params(lb, lb["x_mid"], wl["post_norm"], lb["normed2"])
+                po = norm_params(lb, lb["x_mid"], wl["post_norm"], lb["normed2"],
+                                 fused=fuse)
             add_task(t.id, gi, L.OP_RMSNORM, level, None, wait, t.signal_event,
                      po, layer, n_items=B, n_units=u_rows)
         elif op in (OpKind.QKV_PROJ, OpKind.O_PROJ_RESIDUAL,
@@ -229,10 +253,13 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
             M, K, N = t.gemm_shape
             tile = tuple(t.tile_shape)
             x_in = bufs.x_in0 if layer == 0 else bufs.layers[layer - 1]["x_out"]
+            gamma = None
             if op is OpKind.QKV_PROJ:
                 w, x, y, res, epi, ldx, ldy = (bufs.w_packed[layer]["qkv"],
                                               lb["normed1"], lb["qkv_out"], None,
                                               L.EPI_NONE, d, spec.qkv_dim)
+                if fuse:
+                    x, gamma = x_in, wl["in_norm"]
             elif op is OpKind.O_PROJ_RESIDUAL:
                 w, x, y, res, epi, ldx, ldy = (bufs.w_packed[layer]["o"],
                                               lb["attn_out"], lb["x_mid"], x_in,
@@ -241,6 +268,8 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                 fused = t.level is TaskLevel.CHIPLET
                 w = bufs.w_packed[layer]["gate_up"]
                 x, ldx = lb["normed2"], d
+                if fuse:
+                    x, gamma = lb["x_mid"], wl["post_norm"]
                 if fused:
                     y, epi, ldy = lb["silu_out"], L.EPI_SILU, F
                 else:
@@ -257,14 +286,14 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                 col0 = xd * (n_loc // 2 if epi == L.EPI_SILU else n_loc)
                 po = gemm_params(_ptr(w, xd * n_loc * K), _ptr(x), _ptr(y),
                                  _ptr(res), M, K, n_loc, tile, ldx, ldy, d,
-                                 col0, epi, xd)
+                                 col0, epi, xd, gamma=gamma)
                 add_task(t.id, gi, L.OP_GEMM, level, xd, wait, t.signal_event,
                          po, layer, n_items=0)
             else:
                 work = t.work
                 po = gemm_params(_ptr(w), _ptr(x), _ptr(y), _ptr(res), M, K, N,
                                  tile, ldx, ldy, d, 0, epi, 0,
-                                 tm=work.m_idx, tn=work.n_idx)
+                                 tm=work.m_idx, tn=work.n_idx, gamma=gamma)
                 add_task(t.id, gi, L.OP_GEMM, level, None, wait, t.signal_event,
                          po, layer)
         elif op is OpKind.ATTN_PARTIAL:
@@ -295,8 +324,10 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         ev_index[e] = len(event_names)
         event_names.append(e)
         required.append(0)
-    po = norm_params(None, bufs.layers[n_layers - 1]["x_out"], bufs.final_norm,
-                     bufs.final_normed)
+    x_last = bufs.layers[n_layers - 1]["x_out"]
+    po = norm_params(None, x_last, bufs.final_norm, bufs.final_normed, fused=fuse)
+    lm_x = x_last if fuse else bufs.final_normed
+    lm_gamma = bufs.final_norm if fuse else None
     add_task("final_norm.t0", -1, L.OP_RMSNORM, L.LEVEL_CU, None, last_event,
              "e.final_norm", po, n_layers, n_items=B, n_units=u_rows)
     required[ev_index["e.final_norm"]] = 1
@@ -308,10 +339,10 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         n_loc = V // X
         for xd in range(X):
             po = gemm_params(_ptr(bufs.lm_packed, xd * n_loc * d),
-                             _ptr(bufs.final_normed), _ptr(logits), None,
+                             _ptr(lm_x), _ptr(logits), None,
                              B, d, n_loc, (t_m, t_n, t_k), d, V, d,
                              xd * n_loc, L.EPI_LOGITS, xd,
-                             amax_base=xd * opts.workers)
+                             amax_base=xd * opts.workers, gamma=lm_gamma)
             add_task(f"lm_head.x{xd}", -1, L.OP_GEMM, L.LEVEL_CHIPLET, xd,
                      "e.final_norm", "e.lm_head", po, n_layers, n_items=0)
         required[ev_index["e.lm_head"]] = X
@@ -320,10 +351,10 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         mt, nt = _cdiv(B, t_m), V // t_n
         for m in range(mt):
             for n in range(nt):
-                po = gemm_params(_ptr(bufs.lm_packed), _ptr(bufs.final_normed),
+                po = gemm_params(_ptr(bufs.lm_packed), _ptr(lm_x),
                                  _ptr(logits), None, B, d, V, (t_m, t_n, t_k),
                                  d, V, d, 0, L.EPI_LOGITS, 0, tm=m, tn=n,
-                                 amax_base=n)
+                                 amax_base=n, gamma=lm_gamma)
                 add_task(f"lm_head.t{m * nt + n}", -1, L.OP_GEMM, L.LEVEL_CU,
                          None, "e.final_norm", "e.lm_head", po, n_layers)
         required[ev_index["e.lm_head"]] = mt * nt

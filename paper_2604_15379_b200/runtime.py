@@ -304,13 +304,16 @@ class Megakernel:
             pass
 
 
-def _default_lm_tile(spec: Qwen3Spec, batch: int):
-    t_k = 1024 if spec.hidden % 1024 == 0 else spec.hidden
-    t_k = min(t_k, 1024)
-    t_n = max(1, min(32, 8192 // t_k))
-    while spec.vocab % (2 * t_n):
+def _default_lm_tile(spec: Qwen3Spec, batch: int, t_m: int = 16):
+    """LM-head tile, same rule as analytics.device_tiles (R rows x 8192/R)."""
+    rows = min(batch, t_m)
+    t_n = 16 if rows <= 4 else 32
+    while (spec.vocab // 2) % t_n and t_n > 8:
         t_n //= 2
-    return (16, t_n, t_k)
+    t_k = spec.hidden if spec.hidden < 256 else min(8192 // t_n, spec.hidden)
+    while spec.hidden % t_k:
+        t_k //= 2
+    return (t_m, t_n, t_k)
 
 
 @dataclass

@@ -51,7 +51,7 @@ def _toy_graph(machine, mode, B, layers=2):
     from paper_2604_15379_b200.analytics import device_tiles
     m = model_preset("toy")
     return build_decoder_layer(m, machine, mode, B,
-                               tile_overrides=device_tiles(m, machine, mode),
+                               tile_overrides=device_tiles(m, machine, mode, B),
                                layers=layers)
 
 
