@@ -156,6 +156,8 @@ def build(args, device):
     del w
     torch.cuda.empty_cache()
     mk.fill_kv_random(CTX)
+    if os.environ.get("MK_DEBUG"):
+        mk.lib.mk_set_debug(mk.h, int(os.environ["MK_DEBUG"], 0))
     mk.set_tokens([(17 * i + 3) % VOCAB for i in range(args.batch)])
     info = {"topology": topology_summary(topo), "probe_ok": probe_ok, "graph_tasks": len(g.tasks),
             "units": len(mk.lowered.units)}

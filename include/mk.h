@@ -168,6 +168,8 @@ typedef struct mk_attn_params {
   int32_t n_splits;    /* splits per row allocated (t_max / S)                */
   int32_t t_max;
   float eps, scale;
+  int32_t sub_splits;  /* warps sharing one (item, head): partial pieces per split */
+  int32_t pad;
 } mk_attn_params;
 
 typedef struct mk_silu_params {

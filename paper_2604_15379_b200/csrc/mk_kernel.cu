@@ -47,11 +47,15 @@ namespace mk {
 
 constexpr int kConsWarps = 8;
 constexpr int kCons = kConsWarps * 32;          // consumer threads
-constexpr int kThreads = kCons + 32;            // + fetch warp
+constexpr int kProdThreads = 128;              // producer warpgroup (warp 0 fetches)
+constexpr int kThreads = kCons + kProdThreads;  // 12 warps = 3 warpgroups
+constexpr int kProdRegs = 88;                   // setmaxnreg budget: 128*88 + 256*200
+constexpr int kConsRegs = 200;                  //   = 62464 <= 65536
 constexpr int kSlotBytes = 16384;
 constexpr int kSlots = 10;
 constexpr int kXsBytes = 32768;                 // staged activations per task
 constexpr int kMaxSplits = 128;                 // split-KV splits per row
+constexpr int kMaxPieces = 512;                 // splits x token subsets
 constexpr int kTQ = 32;                         // smem unit queue depth
 constexpr int kMailbox = 64;                    // mailbox depth per worker
 constexpr uint32_t kEnd = 0xFFFFFFu;
@@ -97,10 +101,8 @@ struct KArgs {
 };
 
 struct AttnScratch {
-  float vec[8][128];                // rotated q per head
-  float kn[128], vn[128];           // new token k / v
-  float st[8][288];                 // per-(warp,token-group) state; prologue scratch
-  float wsplit[8][kMaxSplits];      // reduce: per-(head, split) weights
+  float wpiece[8][kMaxPieces];      // reduce: per-(head, piece) m -> weight
+  float lpiece[8][kMaxPieces];      // reduce: per-(head, piece) l
 };
 
 struct Smem {
@@ -216,55 +218,87 @@ struct Ring {
   uint32_t k = 0;   // slots issued / consumed so far this launch
 };
 
-__device__ bool fetch_slot(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
-                           const void* src, uint32_t bytes, uint64_t pol) {
-  const int i = r.k % kSlots;
-  const uint32_t round = r.k / kSlots;
-  if (!mbar_wait(a, &s.empty[i], (round & 1) ^ 1, -2)) return false;
-  if (a.debug & 2) {
-    mbar_arrive(&s.full[i]);
-  } else {
-    mbar_arrive_expect_tx(&s.full[i], bytes);
-    bulk_g2s(ring + size_t(i) * kSlotBytes, src, bytes, &s.full[i], pol);
-  }
-  ++r.k;
-  return true;
-}
+// The sequence of ring slots one unit streams, in consumption order: for a
+// GEMM every K-chunk of every tile this worker owns; for an attention unit
+// the cached K and V block of every item.  Walked twice by the fetch warp:
+// once to prefetch into L2, once to copy into the shared-memory ring.
+struct SlotIter {
+  const mk_task* t;
+  int op, worker, ib, ie;
+  // gemm
+  TileIter it;
+  const __nv_bfloat16* w;
+  int chunks, R, tk, c, cur_n;
+  // attention
+  int item, kv;                 // kv: 0 = K next, 1 = V next
+  const __nv_bfloat16* src_k;
+  uint32_t bytes_kv;
+  bool active;
 
-__device__ bool fetch_unit(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
-                           const mk_task& t, int ib, int ie, int worker, uint64_t pol) {
-  if (t.op == MK_OP_GEMM) {
-    const mk_gemm_params& p = *P<mk_gemm_params>(a, t);
-    const int R = gemm_rows(p);
-    const int chunks = p.K / p.T_K;
-    const uint32_t bytes = uint32_t(R) * p.T_K * 2;
-    TileIter it;
-    it.init(p, a.W, t.level == MK_LEVEL_CHIPLET ? worker : 0);
-    int m, n;
-    const __nv_bfloat16* w = reinterpret_cast<const __nv_bfloat16*>(p.w);
-    while (it.next(m, n)) {
-      const __nv_bfloat16* tile = w + size_t(n) * chunks * R * p.T_K;
-      for (int c = 0; c < chunks; ++c)
-        if (!fetch_slot(a, s, ring, r, tile + size_t(c) * R * p.T_K, bytes, pol)) return false;
+  __device__ void init(const KArgs& a, const mk_task& task, int ib_, int ie_, int worker_) {
+    t = &task; op = task.op; worker = worker_; ib = ib_; ie = ie_; active = true;
+    if (op == MK_OP_GEMM) {
+      const mk_gemm_params& p = *reinterpret_cast<const mk_gemm_params*>(a.params + task.param_off);
+      it.init(p, a.W, task.level == MK_LEVEL_CHIPLET ? worker : 0);
+      w = reinterpret_cast<const __nv_bfloat16*>(p.w);
+      R = gemm_rows(p); tk = p.T_K; chunks = p.K / p.T_K; c = chunks; cur_n = 0;
+    } else if (op == MK_OP_ATTN_PARTIAL) {
+      item = ib; kv = 0; bytes_kv = 0; src_k = nullptr;
+    } else {
+      active = false;
     }
-  } else if (t.op == MK_OP_ATTN_PARTIAL) {
-    const mk_attn_params& p = *P<mk_attn_params>(a, t);
-    for (int i = ib; i < ie; ++i) {
-      const int b = i / p.n_splits, sp = i % p.n_splits;
+  }
+  // next slot: (src, bytes); false when the unit has no more slots
+  __device__ bool next(const KArgs& a, const void*& src, uint32_t& bytes) {
+    if (!active) return false;
+    if (op == MK_OP_GEMM) {
+      if (c >= chunks) {
+        int m, n;
+        if (!it.next(m, n)) { active = false; return false; }
+        cur_n = n; c = 0;
+      }
+      src = w + (size_t(cur_n) * chunks + c) * R * tk;
+      bytes = uint32_t(R) * tk * 2;
+      ++c;
+      return true;
+    }
+    const mk_attn_params& p = *reinterpret_cast<const mk_attn_params*>(a.params + t->param_off);
+    if (kv == 1) {   // V block of the current item
+      src = reinterpret_cast<const __nv_bfloat16*>(p.v_cache) +
+            (reinterpret_cast<const __nv_bfloat16*>(src_k) - reinterpret_cast<const __nv_bfloat16*>(p.k_cache));
+      bytes = bytes_kv; kv = 0; ++item;
+      return true;
+    }
+    for (; item < ie; ++item) {
+      const int b = item / p.n_splits, sp = item % p.n_splits;
       const int pos = p.positions[b];
       const int t0 = sp * p.split;
       if (t0 > pos) continue;
       const int nc = min(p.split, pos - t0);
       if (nc <= 0) continue;
       const size_t row = (size_t(b) * p.kv_heads + p.kv_head) * p.t_max + t0;
-      const uint32_t bytes = uint32_t(nc) * p.head_dim * 2;
-      const __nv_bfloat16* kc = reinterpret_cast<const __nv_bfloat16*>(p.k_cache);
-      const __nv_bfloat16* vc = reinterpret_cast<const __nv_bfloat16*>(p.v_cache);
-      if (!fetch_slot(a, s, ring, r, kc + row * p.head_dim, bytes, pol)) return false;
-      if (!fetch_slot(a, s, ring, r, vc + row * p.head_dim, bytes, pol)) return false;
+      src_k = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + row * p.head_dim;
+      bytes_kv = uint32_t(nc) * p.head_dim * 2;
+      src = src_k; bytes = bytes_kv; kv = 1;
+      return true;
     }
+    active = false;
+    return false;
   }
-  return true;
+};
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src), "r"(bytes) : "memory");
 }
 
 // Consumer-side slot handshake.  After an abort the wait just stops (the
@@ -460,7 +494,8 @@ __device__ void gemm_tile(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           if (j >= rpw / 2) continue;
-          const float g = acc[j][b], u = acc[j + rpw / 2 < 4 ? j + rpw / 2 : 3][b];
+          const float g = acc[j][b];
+          const float u = rpw == 2 ? acc[1][b] : (j == 0 ? acc[2][b] : acc[3][b]);
           y[out_col0 + warp + kConsWarps * j] = f2bf(g / (1.f + __expf(-g)) * u);
         }
       } else {
@@ -767,235 +802,314 @@ __device__ void run_rmsnorm(const KArgs& a, Smem& s, const mk_task& t, int ib, i
 // Attention partial: QK-norm + RoPE (+ KV append for the new token) and a
 // split-KV online-softmax partial over cached tokens streamed into the ring.
 // ---------------------------------------------------------------------------
-// One warp: per-head RMSNorm over HD (vector loads), cast, gamma, RoPE.
+// Barrier-free split-KV attention.  Warp w serves q head j = w % G of the
+// kv group and token subset sub = w / G; lane (tg, dl) holds dims
+// [8*dl, 8*dl+8) of token group tg.  Every warp computes its own
+// q_norm + RoPE (and, for the split holding the new token, k_norm + RoPE and
+// v) in registers: the rotate_half partner dims come from lane dl^(LPT/2) by
+// shuffle.  Each warp writes its own partial (m, l, o) as piece
+// split*nsub + sub, so no shared memory and no CTA barrier is needed; the
+// reduce task merges the pieces.
 template <int HD>
-__device__ void head_norm_rope(const uint16_t* src, const uint16_t* gam, float eps,
-                               const float* cs, const float* sn, float* out, int lane,
-                               float* scratch) {
-  constexpr int LN = HD / 8;            // lanes holding 8 elements each
-  const bool act = lane < LN;
-  const uint4 fv = act ? ldg128_cg(src + lane * 8) : make_uint4(0, 0, 0, 0);
-  const uint4 gv = act ? *reinterpret_cast<const uint4*>(gam + lane * 8) : make_uint4(0, 0, 0, 0);
+__device__ __forceinline__ void norm_rope8(const uint16_t* src, const uint16_t* gam, float eps,
+                                           const float* cs, const float* sn, int dl,
+                                           float (&out)[8]) {
+  constexpr int LPT = HD / 8;
+  constexpr int H2 = HD / 2;
+  const uint4 xv = ldg128_cg(src + dl * 8);
+  const uint4 gv = *reinterpret_cast<const uint4*>(gam + dl * 8);
+  const int ci = (dl * 8) % H2;
+  const float4 c0 = *reinterpret_cast<const float4*>(cs + ci);
+  const float4 c1 = *reinterpret_cast<const float4*>(cs + ci + 4);
+  const float4 s0 = *reinterpret_cast<const float4*>(sn + ci);
+  const float4 s1 = *reinterpret_cast<const float4*>(sn + ci + 4);
   float f[8], g[8];
-  unpack8(fv, f);
+  unpack8(xv, f);
   unpack8(gv, g);
   float ss = 0.f;
 #pragma unroll
   for (int e = 0; e < 8; ++e) ss = fmaf(f[e], f[e], ss);
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+  for (int off = LPT >> 1; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
   const float rs = rsqrtf(ss / float(HD) + eps);
-  if (lane < LN) {
+  float xn[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) scratch[lane * 8 + e] = g[e] * bf2f(f2bf(f[e] * rs));
+  for (int e = 0; e < 8; ++e) xn[e] = g[e] * bf2f(f2bf(f[e] * rs));
+  const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+  const float sv[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+  const bool first_half = dl < LPT / 2;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const float partner = __shfl_xor_sync(0xffffffffu, xn[e], LPT / 2);
+    out[e] = first_half ? xn[e] * cv[e] - partner * sv[e] : xn[e] * cv[e] + partner * sv[e];
   }
-  __syncwarp();
-  constexpr int H2 = HD / 2;
-  for (int i = lane; i < H2; i += 32) {
-    const float x1 = scratch[i], x2 = scratch[i + H2];
-    const float c = cs[i], sv = sn[i];
-    out[i] = x1 * c - x2 * sv;
-    out[i + H2] = x2 * c + x1 * sv;
-  }
-  __syncwarp();
 }
 
+__device__ __forceinline__ float ex2(float x) {   // 2^x, -inf -> 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void phase_rec(const KArgs& a, int kind, int item, uint64_t t0, uint64_t t1) {
+  unsigned long long at = atomicAdd(a.log_cursor, 1ull);
+  if ((long long)at >= a.log_cap) return;
+  mk_log_rec& r = a.log[at];
+  r.kind = kind; r.task = -1; r.item_begin = item; r.worker = -1;
+  r.smid = (int)smid(); r.die = -1; r.t_start = t0; r.t_end = t1;
+}
+
+// One pass = up to 8/G items: warp w serves item (w / G) of the pass and q
+// head (w % G) of the kv group over the item's whole split, 8 tokens per
+// lane group per iteration (independent dot/shuffle/exp chains).  The warp
+// writes its head's partial (m, l, o) directly -- no shared memory, no CTA
+// barrier.  Every warp arrives on every ring slot of the pass.
 template <int HD>
-__device__ void attn_item(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
-                          const mk_attn_params& p, int item, int ct, int& q_row) {
-  AttnScratch& at = s.u.at;
-  const int b = item / p.n_splits, sp = item % p.n_splits;
-  const int pos = p.positions[b];
-  const int t0 = sp * p.split;
-  if (t0 > pos) return;
-  const int nc = min(p.split, pos - t0);
-  const bool has_new = pos < t0 + p.split;
+__device__ void attn_pass(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
+                          const mk_attn_params& p, int i0, int i1, int ct) {
+  constexpr int LPT = HD / 8;          // lanes per token
+  constexpr int TPI = 32 / LPT;        // tokens per warp per sub-step
+  constexpr int CH = 4;                // tokens per lane group per iteration
   const int G = p.group;
+  const int nsub = p.sub_splits;       // warps sharing one (item, head)
   const int warp = ct >> 5, lane = ct & 31;
+  const int head = warp % G, sub = (warp / G) % nsub, slot_item = warp / (G * nsub);
+  const int tg = lane / LPT, dl = lane % LPT;
+  const bool trace = a.log != nullptr && ct == 0;
+  const uint64_t ph0 = trace ? globaltimer() : 0;
+
+  // this warp's item and the ring slots of every item in the pass
+  int my_slot = -1, n_slots = 0;
+  int item = -1, pos = 0, t0 = 0, nc = 0;
+  bool has_new = false;
+  for (int it = i0; it < i1; ++it) {
+    const int b = it / p.n_splits, sp = it % p.n_splits;
+    const int ps = p.positions[b];
+    const int tt0 = sp * p.split;
+    const int nci = tt0 > ps ? 0 : min(p.split, ps - tt0);
+    if (it - i0 == slot_item) {
+      item = it; pos = ps; t0 = tt0; nc = nci;
+      has_new = tt0 <= ps && ps < tt0 + p.split;
+      if (nci > 0) my_slot = n_slots;
+    }
+    if (nci > 0) n_slots += 2;
+  }
+  const bool active = item >= 0 && t0 <= pos;
+  const int b = active ? item / p.n_splits : 0;
+  const int sp = active ? item % p.n_splits : 0;
+
+  float q8[8];
   const uint16_t* qkv = reinterpret_cast<const uint16_t*>(p.qkv) + size_t(b) * p.ldqkv;
   const float* cs = p.rope_cos + size_t(pos) * (HD / 2);
   const float* sn = p.rope_sin + size_t(pos) * (HD / 2);
-
-  // prologue (once per batch row within a unit): q heads of this group
-  // (warps 0..G-1); the new token's k/v by warp G (or after a barrier)
-  const bool need_q = q_row != b;
-  if (need_q && warp < G) {
-    const int qh = p.kv_head * G + warp;
-    head_norm_rope<HD>(qkv + qh * HD, reinterpret_cast<const uint16_t*>(p.q_gamma), p.eps,
-                       cs, sn, at.vec[warp], lane, at.st[warp]);
-  }
-  if (has_new) {
-    const int kw = G < kConsWarps ? G : 0;
-    if (G == kConsWarps) bar_sync(1, kCons);
-    if (warp == kw) {
-      const int koff = p.q_heads * HD + p.kv_head * HD;
-      const int voff = (p.q_heads + p.kv_heads) * HD + p.kv_head * HD;
-      head_norm_rope<HD>(qkv + koff, reinterpret_cast<const uint16_t*>(p.k_gamma), p.eps,
-                         cs, sn, at.kn, lane, at.st[kw]);
-      const size_t crow = ((size_t(b) * p.kv_heads + p.kv_head) * p.t_max + pos) * HD;
-      uint16_t* kc = reinterpret_cast<uint16_t*>(p.k_cache) + crow;
-      uint16_t* vc = reinterpret_cast<uint16_t*>(p.v_cache) + crow;
-      for (int d = lane; d < HD; d += 32) {
-        const uint16_t vv = ldg16_cg(qkv + voff + d);
-        const uint16_t kb = f2bf(at.kn[d]);
-        at.vn[d] = bf2f(vv);
-        kc[d] = kb;
-        vc[d] = vv;
-        at.kn[d] = bf2f(kb);     // attend to the rounded (cached) key, as later steps will
-      }
-    }
-  }
-  q_row = b;
-  bar_sync(1, kCons);
-
-  constexpr int LPT = HD / 8;          // lanes per token
-  constexpr int TPI = 32 / LPT;        // tokens per warp iteration
-  const int head = warp % G, sub = warp / G, nsub = kConsWarps / G;
-  const int tg = lane / LPT, dl = lane % LPT;
-  const float qscale = p.scale * 1.4426950408889634f;
-  float q8[8];
+  if (active) {
+    norm_rope8<HD>(qkv + (p.kv_head * G + head) * HD, reinterpret_cast<const uint16_t*>(p.q_gamma),
+                   p.eps, cs, sn, dl, q8);
+    const float qscale = p.scale * 1.4426950408889634f;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) q8[e] = at.vec[head][dl * 8 + e] * qscale;
-
-  const uint8_t* kslot = nullptr;
-  const uint8_t* vslot = nullptr;
-  if (nc > 0) {
-    cons_wait_slot(a, s, r);
-    kslot = ring + size_t(r.k % kSlots) * kSlotBytes;
-    Ring r2 = r; ++r2.k;
-    cons_wait_slot(a, s, r2);
-    vslot = ring + size_t(r2.k % kSlots) * kSlotBytes;
+    for (int e = 0; e < 8; ++e) q8[e] *= qscale;
   }
+  const uint64_t ph1 = trace ? globaltimer() : 0;
+  uint32_t kslot = 0, vslot = 0;
+  if (active && my_slot >= 0) {
+    Ring rk = r; rk.k += my_slot;
+    cons_wait_slot(a, s, rk);
+    kslot = smem_u32(ring) + uint32_t(rk.k % kSlots) * kSlotBytes;
+    Ring rv = rk; ++rv.k;
+    cons_wait_slot(a, s, rv);
+    vslot = smem_u32(ring) + uint32_t(rv.k % kSlots) * kSlotBytes;
+  }
+  const uint64_t ph2 = trace ? globaltimer() : 0;
   float mx = -INFINITY, l = 0.f, o[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) o[e] = 0.f;
-  const int ntot = nc + (has_new ? 1 : 0);
-  for (int tb = sub * TPI; tb < ntot; tb += nsub * TPI) {
-    const int tk = tb + tg;
-    const bool valid = tk < ntot;
-    float kf[8], vf[8];
-    if (valid && tk < nc) {
-      unpack8(lds128(kslot + size_t(tk) * HD * 2 + dl * 16), kf);
-      unpack8(lds128(vslot + size_t(tk) * HD * 2 + dl * 16), vf);
-    } else {
+  // cached tokens only: TPI*CH per warp step, tail masked
+  const int ncached = active ? nc : 0;
+  for (int tb = sub * TPI * CH; tb < ncached; tb += nsub * TPI * CH) {
+    float sc[CH];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        kf[e] = valid ? at.kn[dl * 8 + e] : 0.f;
-        vf[e] = valid ? at.vn[dl * 8 + e] : 0.f;
+    for (int c = 0; c < CH; ++c) {
+      const int tk = tb + c * TPI + tg;
+      uint4 k4 = make_uint4(0, 0, 0, 0);
+      if (tk < ncached)
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(k4.x), "=r"(k4.y), "=r"(k4.z), "=r"(k4.w)
+                     : "r"(kslot + uint32_t(tk * HD * 2 + dl * 16)) : "memory");
+      float acc = q8[0] * bf16lo(k4.x);
+      acc = fmaf(q8[1], bf16hi(k4.x), acc);
+      acc = fmaf(q8[2], bf16lo(k4.y), acc);
+      acc = fmaf(q8[3], bf16hi(k4.y), acc);
+      acc = fmaf(q8[4], bf16lo(k4.z), acc);
+      acc = fmaf(q8[5], bf16hi(k4.z), acc);
+      acc = fmaf(q8[6], bf16lo(k4.w), acc);
+      acc = fmaf(q8[7], bf16hi(k4.w), acc);
+      sc[c] = acc;
+    }
+#pragma unroll
+    for (int off = LPT >> 1; off > 0; off >>= 1)
+#pragma unroll
+      for (int c = 0; c < CH; ++c) sc[c] += __shfl_xor_sync(0xffffffffu, sc[c], off);
+    float cm = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (tb + c * TPI + tg >= ncached) sc[c] = -INFINITY;
+      cm = fmaxf(cm, sc[c]);
+    }
+    const float mn = fmaxf(mx, cm);
+    if (mn != -INFINITY) {
+      const float corr = ex2(mx - mn);
+      l *= corr;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] *= corr;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int tk = tb + c * TPI + tg;
+        const float pr = ex2(sc[c] - mn);     // 0 for padded tokens
+        l += pr;
+        if (tk < ncached) {
+          uint4 v4;
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(v4.x), "=r"(v4.y), "=r"(v4.z), "=r"(v4.w)
+                       : "r"(vslot + uint32_t(tk * HD * 2 + dl * 16)) : "memory");
+          o[0] = fmaf(pr, bf16lo(v4.x), o[0]); o[1] = fmaf(pr, bf16hi(v4.x), o[1]);
+          o[2] = fmaf(pr, bf16lo(v4.y), o[2]); o[3] = fmaf(pr, bf16hi(v4.y), o[3]);
+          o[4] = fmaf(pr, bf16lo(v4.z), o[4]); o[5] = fmaf(pr, bf16hi(v4.z), o[5]);
+          o[6] = fmaf(pr, bf16lo(v4.w), o[6]); o[7] = fmaf(pr, bf16hi(v4.w), o[7]);
+        }
       }
+      mx = mn;
+    }
+  }
+  // the token being decoded: k_norm + RoPE and v from the qkv row, appended
+  // to the cache, folded into token group 0 of the sub-0 warp
+  if (active && has_new) {
+    float kn[8];
+    norm_rope8<HD>(qkv + p.q_heads * HD + p.kv_head * HD,
+                   reinterpret_cast<const uint16_t*>(p.k_gamma), p.eps, cs, sn, dl, kn);
+    const uint4 vv = ldg128_cg(qkv + (p.q_heads + p.kv_heads) * HD + p.kv_head * HD + dl * 8);
+    uint16_t kb[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { kb[e] = f2bf(kn[e]); kn[e] = bf2f(kb[e]); }   // attend to the cached key
+    if (head == 0 && sub == 0 && tg == 0) {
+      const size_t crow = ((size_t(b) * p.kv_heads + p.kv_head) * p.t_max + pos) * HD + dl * 8;
+      *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.k_cache) + crow) = *reinterpret_cast<uint4*>(kb);
+      *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.v_cache) + crow) = vv;
     }
     float sc = 0.f;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) sc = fmaf(q8[e], kf[e], sc);
+    for (int e = 0; e < 8; ++e) sc = fmaf(q8[e], kn[e], sc);
 #pragma unroll
     for (int off = LPT >> 1; off > 0; off >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, off);
-    if (valid) {
+    if (sub == 0 && tg == 0) {
+      float vf[8];
+      unpack8(vv, vf);
       const float mn = fmaxf(mx, sc);
-      const float corr = exp2f(mx - mn);
-      const float pr = exp2f(sc - mn);
+      const float corr = ex2(mx - mn), pr = ex2(sc - mn);
       l = l * corr + pr;
 #pragma unroll
       for (int e = 0; e < 8; ++e) o[e] = fmaf(o[e], corr, pr * vf[e]);
       mx = mn;
     }
   }
-  if (nc > 0) {
-    cons_release_slot(s, r);
-    cons_release_slot(s, r);
-  }
-  // combine the (warp, token-group) states of each head
-  bar_sync(1, kCons);            // prologue scratch (st) no longer read
-  float* st = at.st[warp] + tg * (HD + 2);
+  for (int k = 0; k < n_slots; ++k) cons_release_slot(s, r);
+  // merge the warp's token groups (lanes tg and tg' hold the same dims)
 #pragma unroll
-  for (int e = 0; e < 8; ++e) st[dl * 8 + e] = o[e];
-  if (dl == 0) { st[HD] = mx; st[HD + 1] = l; }
-  bar_sync(1, kCons);
-  float* part = p.partial + ((size_t(b) * p.kv_heads + p.kv_head) * p.n_splits + sp) * G * (HD + 4);
-  for (int e = ct; e < G * HD; e += kCons) {
-    const int hh = e / HD, d = e % HD;
-    float M = -INFINITY;
-    for (int q = 0; q < nsub; ++q)
-      for (int g2 = 0; g2 < TPI; ++g2) M = fmaxf(M, at.st[q * G + hh][g2 * (HD + 2) + HD]);
-    float acc = 0.f, den = 0.f;
-    for (int q = 0; q < nsub; ++q)
-      for (int g2 = 0; g2 < TPI; ++g2) {
-        const float* x = at.st[q * G + hh] + g2 * (HD + 2);
-        if (x[HD] == -INFINITY) continue;
-        const float f = exp2f(x[HD] - M);
-        acc = fmaf(f, x[d], acc);
-        den = fmaf(f, x[HD + 1], den);
-      }
-    float* dst = part + size_t(hh) * (HD + 4);
-    dst[d] = acc;
-    if (d == 0) { dst[HD] = M; dst[HD + 1] = den; }
+  for (int off = LPT; off < 32; off <<= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, mx, off);
+    const float l2 = __shfl_xor_sync(0xffffffffu, l, off);
+    const float mn = fmaxf(mx, m2);
+    const float f1 = mn == -INFINITY ? 0.f : exp2f(mx - mn);
+    const float f2 = mn == -INFINITY ? 0.f : exp2f(m2 - mn);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float o2 = __shfl_xor_sync(0xffffffffu, o[e], off);
+      o[e] = o[e] * f1 + o2 * f2;
+    }
+    l = l * f1 + l2 * f2;
+    mx = mn;
   }
-  bar_sync(1, kCons);
+  const uint64_t ph3 = trace ? globaltimer() : 0;
+  if (active && tg == 0) {
+    const int piece = sp * nsub + sub;
+    float* dst = p.partial + (((size_t(b) * p.kv_heads + p.kv_head) * p.n_splits * nsub + piece) * G + head) * (HD + 4);
+    *reinterpret_cast<float4*>(dst + dl * 8) = make_float4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<float4*>(dst + dl * 8 + 4) = make_float4(o[4], o[5], o[6], o[7]);
+    if (dl == 0) { dst[HD] = mx; dst[HD + 1] = l; }
+  }
+  if (trace) {
+    phase_rec(a, 2, i0, ph0, ph1);       // prologue (q/k norm + rope)
+    phase_rec(a, 3, i0, ph1, ph2);       // waiting for the K/V slots
+    phase_rec(a, 4, i0, ph2, ph3);       // token loop
+  }
 }
 
 __device__ void run_attn_partial(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
                                  const mk_task& t, int ib, int ie, int ct) {
   const mk_attn_params& p = *P<mk_attn_params>(a, t);
-  int q_row = -1;
-  for (int i = ib; i < ie; ++i) {
+  const int per = kConsWarps / (p.group * p.sub_splits);
+  for (int i = ib; i < ie; i += per) {
+    const int i1 = min(ie, i + per);
     switch (p.head_dim) {
-      case 128: attn_item<128>(a, s, ring, r, p, i, ct, q_row); break;
-      case 64: attn_item<64>(a, s, ring, r, p, i, ct, q_row); break;
-      case 32: attn_item<32>(a, s, ring, r, p, i, ct, q_row); break;
-      default: attn_item<16>(a, s, ring, r, p, i, ct, q_row); break;
+      case 128: attn_pass<128>(a, s, ring, r, p, i, i1, ct); break;
+      case 64: attn_pass<64>(a, s, ring, r, p, i, i1, ct); break;
+      case 32: attn_pass<32>(a, s, ring, r, p, i, i1, ct); break;
+      default: attn_pass<16>(a, s, ring, r, p, i, i1, ct); break;
     }
   }
 }
 
-// Merge the split partials of one kv head for rows [ib, ie): all (head, split)
-// maxima load in parallel, then every (head, dim) thread streams its splits.
+// Merge the split partials of one kv head for rows [ib, ie).  Thread
+// (head, dims) loads every split's m and l, forms the weights itself and
+// streams the o values -- two rounds of independent loads, no barrier.
 __device__ void run_attn_reduce(const KArgs& a, Smem& s, const mk_task& t, int ib, int ie, int ct) {
   const mk_attn_params& p = *P<mk_attn_params>(a, t);
-  AttnScratch& at = s.u.at;
   const int HD = p.head_dim, G = p.group;
+  const int stride = G * (HD + 4);          // floats per piece
   uint16_t* out = reinterpret_cast<uint16_t*>(p.out);
+  constexpr int kBatch = 16;
   for (int b = ib; b < ie; ++b) {
     const int pos = p.positions[b];
-    const int nv = min(pos / p.split + 1, kMaxSplits);
-    const float* base = p.partial + (size_t(b) * p.kv_heads + p.kv_head) * p.n_splits * G * (HD + 4);
-    // weights: w[h][s] = exp2(m_s - M_h) for every split; the denominator
-    // sum_s w*l goes into slot kMaxSplits-1's neighbour via a second pass
-    for (int e = ct; e < G * nv; e += kCons) {
-      const int hh = e / nv, sp = e % nv;
-      at.wsplit[hh][sp] = __ldcg(base + (size_t(sp) * G + hh) * (HD + 4) + HD);
-    }
-    bar_sync(1, kCons);
-    if (ct < G) {
+    const int nv = (pos / p.split + 1) * p.sub_splits;   // pieces written this step
+    const float* base = p.partial + (size_t(b) * p.kv_heads + p.kv_head) * p.n_splits * p.sub_splits * stride;
+    for (int e = ct; e < G * HD / 4; e += kCons) {   // 4 dims per thread
+      const int hh = (e * 4) / HD, d = (e * 4) % HD;
+      const float* hb = base + hh * (HD + 4);
       float M = -INFINITY;
-      for (int sp = 0; sp < nv; ++sp) M = fmaxf(M, at.wsplit[ct][sp]);
+      for (int s0 = 0; s0 < nv; s0 += kBatch) {
+        float mv[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) mv[u] = (s0 + u < nv) ? __ldcg(hb + size_t(s0 + u) * stride + HD) : -INFINITY;
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) M = fmaxf(M, mv[u]);
+      }
       float den = 0.f;
-      for (int sp = 0; sp < nv; ++sp) {
-        const float w = exp2f(at.wsplit[ct][sp] - M);
-        den = fmaf(w, __ldcg(base + (size_t(sp) * G + ct) * (HD + 4) + HD + 1), den);
-        at.wsplit[ct][sp] = w;
+      float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s0 = 0; s0 < nv; s0 += kBatch) {
+        float mv[kBatch], lv[kBatch];
+        float4 ov[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const bool ok = s0 + u < nv;
+          const float* x = hb + size_t(s0 + u) * stride;
+          mv[u] = ok ? __ldcg(x + HD) : -INFINITY;
+          lv[u] = ok ? __ldcg(x + HD + 1) : 0.f;
+          ov[u] = ok ? __ldcg(reinterpret_cast<const float4*>(x + d)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const float w = mv[u] == -INFINITY ? 0.f : exp2f(mv[u] - M);
+          den = fmaf(w, lv[u], den);
+          num.x = fmaf(w, ov[u].x, num.x); num.y = fmaf(w, ov[u].y, num.y);
+          num.z = fmaf(w, ov[u].z, num.z); num.w = fmaf(w, ov[u].w, num.w);
+        }
       }
-      s.bred[ct] = 1.f / den;
+      const float inv = 1.f / den;
+      uint16_t o4[4] = {f2bf(num.x * inv), f2bf(num.y * inv), f2bf(num.z * inv), f2bf(num.w * inv)};
+      *reinterpret_cast<uint2*>(out + size_t(b) * p.q_heads * HD + (p.kv_head * G + hh) * HD + d) =
+          *reinterpret_cast<uint2*>(o4);
     }
-    bar_sync(1, kCons);
-    for (int e = ct; e < G * HD; e += kCons) {
-      const int hh = e / HD, d = e % HD;
-      const float* col = base + size_t(hh) * (HD + 4) + d;
-      float num = 0.f;
-      int sp = 0;
-      for (; sp + 4 <= nv; sp += 4) {
-        const float o0 = __ldcg(col + size_t(sp) * G * (HD + 4));
-        const float o1 = __ldcg(col + size_t(sp + 1) * G * (HD + 4));
-        const float o2 = __ldcg(col + size_t(sp + 2) * G * (HD + 4));
-        const float o3 = __ldcg(col + size_t(sp + 3) * G * (HD + 4));
-        num = fmaf(at.wsplit[hh][sp], o0, num);
-        num = fmaf(at.wsplit[hh][sp + 1], o1, num);
-        num = fmaf(at.wsplit[hh][sp + 2], o2, num);
-        num = fmaf(at.wsplit[hh][sp + 3], o3, num);
-      }
-      for (; sp < nv; ++sp) num = fmaf(at.wsplit[hh][sp], __ldcg(col + size_t(sp) * G * (HD + 4)), num);
-      out[size_t(b) * p.q_heads * HD + (p.kv_head * G + hh) * HD + d] = f2bf(num * s.bred[hh]);
-    }
-    bar_sync(1, kCons);
   }
+  (void)s;
 }
 
 __device__ void run_silu(const KArgs& a, const mk_task& t, int ct) {
@@ -1120,34 +1234,35 @@ __device__ void scheduler(const KArgs& a, SchedSmem& s, int g) {
   }
 }
 
-__device__ void fetch_warp(const KArgs& a, Smem& s, uint8_t* ring, int g, int worker) {
+// Producer warpgroup, two single-lane roles that never wait on task
+// dependencies (weights and past KV blocks are immutable during the step):
+//  * mailbox warp (warp 1): scheduler mailbox -> unit queue tq;
+//  * ring warp (warp 0): walks the queued units' slot streams and TMA-copies
+//    each slot into the next free shared-memory ring slot.
+// Splitting them keeps the mailbox's L2 round trips off the ring refill path.
+__device__ void mailbox_warp(const KArgs& a, Smem& s, int g, int worker) {
   if ((threadIdx.x & 31) != 0) return;
   const int gw = g * a.W + worker;
   uint64_t head = a.mb_head[gw];
-  const uint64_t pol = policy_evict_first();
-  Ring r;
-  uint32_t q = 0;
-  for (;;) {
-    uint64_t e;
-    Spin sp;
-    const uint64_t* slotp = &a.mailbox[size_t(gw) * kMailbox + head % kMailbox];
-    for (;;) {
-      e = ld_acquire64(slotp);
-      if ((e >> 24) == head + 1) break;
-      if (!sp.ok(a, -5)) { e = kEnd; break; }
+  for (uint32_t q = 0;; ++q) {
+    const int qi = q % kTQ;
+    const bool room = mbar_wait(a, &s.tq_empty[qi], ((q / kTQ) & 1) ^ 1, -6);
+    uint64_t e = kEnd;
+    if (room) {
+      Spin sp;
+      const uint64_t* slotp = &a.mailbox[size_t(gw) * kMailbox + head % kMailbox];
+      for (;;) {
+        e = ld_acquire64(slotp);
+        if ((e >> 24) == head + 1) break;
+        if (!sp.ok(a, -5)) { e = kEnd; break; }
+      }
+      if ((e >> 24) == head + 1) {
+        ++head;
+        st_release64(&a.mb_head[gw], head);
+      }
     }
     const uint32_t payload = uint32_t(e & 0xFFFFFFu);
-    if ((e >> 24) == head + 1) {
-      ++head;
-      st_release64(&a.mb_head[gw], head);
-    }
-    const int qi = q % kTQ;
-    if (!mbar_wait(a, &s.tq_empty[qi], ((q / kTQ) & 1) ^ 1, -6)) {
-      s.tq[qi] = make_int4(-1, 0, 0, 0);
-      mbar_arrive(&s.tq_full[qi]);
-      return;
-    }
-    if (payload == kEnd) {
+    if (payload == kEnd || !room) {
       s.tq[qi] = make_int4(-1, 0, 0, 0);
       mbar_arrive(&s.tq_full[qi]);
       return;
@@ -1155,16 +1270,38 @@ __device__ void fetch_warp(const KArgs& a, Smem& s, uint8_t* ring, int g, int wo
     const mk_unit u = a.units[payload];
     s.tq[qi] = make_int4(u.task, u.item_begin, u.item_end, 0);
     mbar_arrive(&s.tq_full[qi]);
-    ++q;
-    if (!fetch_unit(a, s, ring, r, a.tasks[u.task], u.item_begin, u.item_end, worker, pol)) {
-      // aborted: make sure the consumers see an end marker eventually
-      return;
+  }
+}
+
+__device__ void ring_warp(const KArgs& a, Smem& s, uint8_t* ring, int worker) {
+  if ((threadIdx.x & 31) != 0) return;
+  const uint64_t pol = policy_evict_first();
+  uint32_t slot = 0;
+  for (uint32_t q = 0;; ++q) {
+    const int qi = q % kTQ;
+    if (!mbar_wait(a, &s.tq_full[qi], (q / kTQ) & 1, -8)) return;
+    const int4 ent = s.tq[qi];
+    if (ent.x < 0) return;
+    SlotIter it;
+    it.init(a, a.tasks[ent.x], ent.y, ent.z, worker);
+    const void* src;
+    uint32_t bytes;
+    while (it.next(a, src, bytes)) {
+      const int i = slot % kSlots;
+      if (!mbar_wait(a, &s.empty[i], ((slot / kSlots) & 1) ^ 1, -2)) return;
+      if (a.debug & 2) {
+        mbar_arrive(&s.full[i]);
+      } else {
+        mbar_arrive_expect_tx(&s.full[i], bytes);
+        bulk_g2s(ring + size_t(i) * kSlotBytes, src, bytes, &s.full[i], pol);
+      }
+      ++slot;
     }
   }
 }
 
 __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int worker) {
-  const int ct = threadIdx.x - 32;
+  const int ct = threadIdx.x - kProdThreads;
   const int gw = g * a.W + worker;
   Ring r;
   uint32_t q = 0;
@@ -1278,8 +1415,16 @@ __global__ void __launch_bounds__(kThreads, 1) megakernel(const KArgs a) {
   }
   const int worker = rank - 1;
   if (worker >= a.W) return;             // extra SMs of the larger die idle
-  if (threadIdx.x < 32) fetch_warp(a, s, ring, g, worker);
-  else consumers(a, s, ring, g, worker);
+  // warp specialisation with register reallocation: the producer warpgroup
+  // drops to kProdRegs, the two consumer warpgroups grow to kConsRegs
+  if (threadIdx.x < kProdThreads) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(kProdRegs));
+    if (threadIdx.x < 32) ring_warp(a, s, ring, worker);
+    else if (threadIdx.x < 64) mailbox_warp(a, s, g, worker);
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(kConsRegs));
+    consumers(a, s, ring, g, worker);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1559,7 +1704,9 @@ static int validate_graph(const mk_graph_desc* g) {
           static_cast<const uint8_t*>(g->params) + t.param_off);
       const int hd = p->head_dim;
       if ((hd != 16 && hd != 32 && hd != 64 && hd != 128) || p->group < 1 || p->group > 8 ||
-          8 % p->group || size_t(p->split) * hd * 2 > size_t(kSlotBytes) || p->n_splits > kMaxSplits)
+          8 % p->group || size_t(p->split) * hd * 2 > size_t(kSlotBytes) ||
+          p->n_splits > kMaxSplits || p->sub_splits < 1 || p->group * p->sub_splits > kConsWarps ||
+          kConsWarps % (p->group * p->sub_splits))
         return fail(MK_ERR_CONFIG, "attention task " + std::to_string(i) + " has unsupported shapes");
     }
   }

@@ -213,6 +213,9 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         p.group, p.kv_head = spec.group, h
         p.split, p.n_splits, p.t_max = bufs.split, bufs.n_splits, bufs.t_max
         p.eps, p.scale = spec.eps, hd ** -0.5
+        # one item per unit (small batch): two warps share each (item, head)
+        # and write two partial pieces; otherwise one warp per (item, head)
+        p.sub_splits = 2 if (B * bufs.n_splits <= u_attn and 8 % (2 * spec.group) == 0) else 1
         return blob.add(p)
 
     def gemm_tile_of(kind):

@@ -169,7 +169,8 @@ def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
         if keep_logits else None
     st.amax_val = torch.zeros(amax_slots, B, device=dev, dtype=torch.float32)
     st.amax_idx = torch.zeros(amax_slots, B, device=dev, dtype=torch.int32)
-    st.partial = torch.zeros(B * sp.kv_heads * n_splits * sp.group * (hd + 4),
+    # pieces: n_splits x (8 warps / group) token subsets, each G x (HD + 4)
+    st.partial = torch.zeros(B * sp.kv_heads * n_splits * 8 * (hd + 4),
                              device=dev, dtype=torch.float32)
     st.tokens = torch.zeros(B, device=dev, dtype=torch.int32)
     st.out_tokens = torch.zeros(B, device=dev, dtype=torch.int32)

@@ -42,6 +42,15 @@ def main():
     recs, n = mk.read_log(cap)
     names = mk.lowered.task_names
     exe = [r for r in recs if r.kind == 1]
+    phases = {}
+    for r in recs:
+        if r.kind in (2, 3, 4):
+            phases.setdefault(r.kind, []).append((r.t_end - r.t_start) / 1e3)
+    for k, name in ((2, "attn prologue"), (3, "attn K/V slot wait"), (4, "attn token loop")):
+        v = phases.get(k, [])
+        if v:
+            v.sort()
+            print(f"{name:>20}: n {len(v)} mean {sum(v)/len(v):.2f} us  p50 {v[len(v)//2]:.2f}  max {v[-1]:.2f}")
     disp = [r for r in recs if r.kind == 0]
     t0 = min(r.t_start for r in exe)
     stage = collections.OrderedDict()
