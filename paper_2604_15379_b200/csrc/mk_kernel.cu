@@ -101,8 +101,7 @@ struct KArgs {
 };
 
 struct AttnScratch {
-  float wpiece[8][kMaxPieces];      // reduce: per-(head, piece) m -> weight
-  float lpiece[8][kMaxPieces];      // reduce: per-(head, piece) l
+  float xch[8][132];                // sub-warp partial state exchange
 };
 
 struct Smem {
@@ -334,6 +333,15 @@ __device__ void stage_x(Smem& s, const mk_gemm_params& p, int m0, int rows, int 
   const uint16_t* x = reinterpret_cast<const uint16_t*>(p.x);
   const int K = p.K;
   const bool norm = p.norm_gamma != nullptr;
+  const uint16_t* gam = reinterpret_cast<const uint16_t*>(p.norm_gamma);
+  constexpr int kSeg = 6;                  // K <= 6 * 2048 per thread pass
+  // gamma is static: issue its loads together with x's (one round trip)
+  uint4 gv[kSeg];
+#pragma unroll
+  for (int q = 0; q < kSeg; ++q) {
+    const int k = ct * 8 + q * kCons * 8;
+    gv[q] = (norm && k < K) ? *reinterpret_cast<const uint4*>(gam + k) : make_uint4(0, 0, 0, 0);
+  }
   float ss[kMaxNB];
 #pragma unroll
   for (int b = 0; b < kMaxNB; ++b) ss[b] = 0.f;
@@ -372,13 +380,15 @@ __device__ void stage_x(Smem& s, const mk_gemm_params& p, int m0, int rows, int 
       s.rs[ct] = rsqrtf(t / float(K) + p.norm_eps);
     }
     bar_sync(1, kCons);
-    const uint16_t* gam = reinterpret_cast<const uint16_t*>(p.norm_gamma);
     for (int b = 0; b < rows; ++b) {
       const float rs = s.rs[b];
-      for (int k = ct * 8; k < K; k += kCons * 8) {
+#pragma unroll
+      for (int q = 0; q < kSeg; ++q) {
+        const int k = ct * 8 + q * kCons * 8;
+        if (k >= K) continue;
         float f[8], g[8];
         unpack8(*reinterpret_cast<const uint4*>(&s.u.xs[b * K + k]), f);
-        unpack8(*reinterpret_cast<const uint4*>(gam + k), g);
+        unpack8(gv[q], g);
         uint16_t o[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) o[e] = f2bf(g[e] * bf2f(f2bf(f[e] * rs)));
@@ -1029,9 +1039,32 @@ __device__ void attn_pass(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
     mx = mn;
   }
   const uint64_t ph3 = trace ? globaltimer() : 0;
-  if (active && tg == 0) {
-    const int piece = sp * nsub + sub;
-    float* dst = p.partial + (((size_t(b) * p.kv_heads + p.kv_head) * p.n_splits * nsub + piece) * G + head) * (HD + 4);
+  if (nsub > 1) {
+    // sub-warps of an (item, head) hand their state to sub 0 through smem
+    float* xch = s.u.at.xch[warp];
+    if (sub > 0 && tg == 0) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) xch[dl * 8 + e] = o[e];
+      if (dl == 0) { xch[HD] = mx; xch[HD + 1] = l; }
+    }
+    bar_sync(1, kCons);
+    if (sub == 0) {
+      for (int k = 1; k < nsub; ++k) {
+        const float* src = s.u.at.xch[warp + k * G];
+        const float m2 = src[HD], l2 = src[HD + 1];
+        const float mn = fmaxf(mx, m2);
+        const float f1 = mn == -INFINITY ? 0.f : ex2(mx - mn);
+        const float f2 = mn == -INFINITY ? 0.f : ex2(m2 - mn);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = o[e] * f1 + src[dl * 8 + e] * f2;
+        l = l * f1 + l2 * f2;
+        mx = mn;
+      }
+    }
+    bar_sync(1, kCons);            // xch reusable by the next pass
+  }
+  if (active && tg == 0 && sub == 0) {
+    float* dst = p.partial + (((size_t(b) * p.kv_heads + p.kv_head) * p.n_splits + sp) * G + head) * (HD + 4);
     *reinterpret_cast<float4*>(dst + dl * 8) = make_float4(o[0], o[1], o[2], o[3]);
     *reinterpret_cast<float4*>(dst + dl * 8 + 4) = make_float4(o[4], o[5], o[6], o[7]);
     if (dl == 0) { dst[HD] = mx; dst[HD + 1] = l; }
@@ -1059,30 +1092,23 @@ __device__ void run_attn_partial(const KArgs& a, Smem& s, uint8_t* ring, Ring& r
 }
 
 // Merge the split partials of one kv head for rows [ib, ie).  Thread
-// (head, dims) loads every split's m and l, forms the weights itself and
-// streams the o values -- two rounds of independent loads, no barrier.
+// (head, 4 dims) streams the splits in batches of 16 -- (m, l, o[4]) of a
+// whole batch in flight -- and merges them online with a running max, so
+// up to 16 splits cost one L2 round trip; no barrier.
 __device__ void run_attn_reduce(const KArgs& a, Smem& s, const mk_task& t, int ib, int ie, int ct) {
   const mk_attn_params& p = *P<mk_attn_params>(a, t);
   const int HD = p.head_dim, G = p.group;
-  const int stride = G * (HD + 4);          // floats per piece
+  const int stride = G * (HD + 4);          // floats per split
   uint16_t* out = reinterpret_cast<uint16_t*>(p.out);
-  constexpr int kBatch = 16;
+  constexpr int kBatch = 20;
   for (int b = ib; b < ie; ++b) {
     const int pos = p.positions[b];
-    const int nv = (pos / p.split + 1) * p.sub_splits;   // pieces written this step
-    const float* base = p.partial + (size_t(b) * p.kv_heads + p.kv_head) * p.n_splits * p.sub_splits * stride;
+    const int nv = pos / p.split + 1;
+    const float* base = p.partial + (size_t(b) * p.kv_heads + p.kv_head) * p.n_splits * stride;
     for (int e = ct; e < G * HD / 4; e += kCons) {   // 4 dims per thread
       const int hh = (e * 4) / HD, d = (e * 4) % HD;
       const float* hb = base + hh * (HD + 4);
-      float M = -INFINITY;
-      for (int s0 = 0; s0 < nv; s0 += kBatch) {
-        float mv[kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) mv[u] = (s0 + u < nv) ? __ldcg(hb + size_t(s0 + u) * stride + HD) : -INFINITY;
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) M = fmaxf(M, mv[u]);
-      }
-      float den = 0.f;
+      float M = -INFINITY, den = 0.f;
       float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int s0 = 0; s0 < nv; s0 += kBatch) {
         float mv[kBatch], lv[kBatch];
@@ -1095,13 +1121,19 @@ __device__ void run_attn_reduce(const KArgs& a, Smem& s, const mk_task& t, int i
           lv[u] = ok ? __ldcg(x + HD + 1) : 0.f;
           ov[u] = ok ? __ldcg(reinterpret_cast<const float4*>(x + d)) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
+        float bm = M;
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) bm = fmaxf(bm, mv[u]);
+        const float corr = M == -INFINITY ? 0.f : ex2(M - bm);
+        den *= corr; num.x *= corr; num.y *= corr; num.z *= corr; num.w *= corr;
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
-          const float w = mv[u] == -INFINITY ? 0.f : exp2f(mv[u] - M);
+          const float w = mv[u] == -INFINITY ? 0.f : ex2(mv[u] - bm);
           den = fmaf(w, lv[u], den);
           num.x = fmaf(w, ov[u].x, num.x); num.y = fmaf(w, ov[u].y, num.y);
           num.z = fmaf(w, ov[u].z, num.z); num.w = fmaf(w, ov[u].w, num.w);
         }
+        M = bm;
       }
       const float inv = 1.f / den;
       uint16_t o4[4] = {f2bf(num.x * inv), f2bf(num.y * inv), f2bf(num.z * inv), f2bf(num.w * inv)};
@@ -1694,7 +1726,7 @@ static int validate_graph(const mk_graph_desc* g) {
           (p->epilogue == MK_EPI_SILU && (R / kConsWarps) % 2) ||
           p->N % R || p->T_M > kMaxNB || (p->epilogue == MK_EPI_LOGITS && p->M > kAmaxRows) ||
           (p->stage_x && size_t(std::min(p->T_M, p->M)) * p->K * 2 > size_t(kXsBytes)) ||
-          (p->norm_gamma && !p->stage_x))
+          (p->norm_gamma && (!p->stage_x || p->K > 6 * 2048)))
         return fail(MK_ERR_CONFIG, "gemm task " + std::to_string(i) + " has an unsupported tile (" +
                                        std::to_string(p->T_M) + "," + std::to_string(p->T_N) + "," +
                                        std::to_string(p->T_K) + ")");

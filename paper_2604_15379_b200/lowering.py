@@ -50,6 +50,8 @@ class LoweringOptions:
     attn_split: int = 64           # tokens per split-KV item
     fuse_norm: bool = True         # RMSNorm folded into the consuming GEMM's
                                    # activation staging when the rows fit
+    bypass_noop: bool = True       # consumers of a fused (no-op) norm task wait
+                                   # on that task's own predecessor event
 
 XS_BYTES = 32768                   # kXsBytes in mk_kernel.cu
 
@@ -228,15 +230,23 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         stages(B, d, tl) for tl in (gemm_tile_of(OpKind.QKV_PROJ),
                                     gemm_tile_of(OpKind.GATE_UP_SILU),
                                     opts.lm_tile))
-    u_attn = _cdiv(total_workers, spec.kv_heads)
+    # attention units: at most one per worker (a second unit on a worker
+    # would serialise behind the first)
+    u_attn = max(1, total_workers // spec.kv_heads)
     u_rows = min(B, 16)
     silu_meta = _silu_meta(g, B, F)
+
+    # event -> event its (no-op) signaller waited on: a fused RMSNorm task
+    # without the L0 embedding gather does no work, so waiting on its event
+    # would only add a completion hop to the critical path
+    bypass = {}
 
     for gi, t in enumerate(g.tasks):
         layer = int(t.id.split(".")[0][1:])
         lb = bufs.layers[layer]
         wl = bufs.w_layers[layer]
         wait = t.wait_events[0] if t.wait_events else None
+        wait = bypass.get(wait, wait)
         level = {TaskLevel.CHIPLET: L.LEVEL_CHIPLET, TaskLevel.CU: L.LEVEL_CU,
                  TaskLevel.WAVEFRONT: L.LEVEL_WAVEFRONT}[t.level]
         op = t.op_kind
@@ -251,6 +261,8 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                                  fused=fuse)
             add_task(t.id, gi, L.OP_RMSNORM, level, None, wait, t.signal_event,
                      po, layer, n_items=B, n_units=u_rows)
+            if fuse and opts.bypass_noop and not (first and layer == 0) and wait:
+                bypass[t.signal_event] = wait
         elif op in (OpKind.QKV_PROJ, OpKind.O_PROJ_RESIDUAL,
                     OpKind.GATE_UP_SILU, OpKind.DOWN_PROJ_RESIDUAL):
             M, K, N = t.gemm_shape
@@ -333,6 +345,7 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
     lm_gamma = bufs.final_norm if fuse else None
     add_task("final_norm.t0", -1, L.OP_RMSNORM, L.LEVEL_CU, None, last_event,
              "e.final_norm", po, n_layers, n_items=B, n_units=u_rows)
+    lm_wait = last_event if (fuse and opts.bypass_noop) else "e.final_norm"
     required[ev_index["e.final_norm"]] = 1
     t_m, t_n, t_k = opts.lm_tile
     V = spec.vocab
@@ -347,7 +360,7 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                              xd * n_loc, L.EPI_LOGITS, xd,
                              amax_base=xd * opts.workers, gamma=lm_gamma)
             add_task(f"lm_head.x{xd}", -1, L.OP_GEMM, L.LEVEL_CHIPLET, xd,
-                     "e.final_norm", "e.lm_head", po, n_layers, n_items=0)
+                     lm_wait, "e.lm_head", po, n_layers, n_items=0)
         required[ev_index["e.lm_head"]] = X
         amax_slots = X * opts.workers
     else:
@@ -359,7 +372,7 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                                  d, V, d, 0, L.EPI_LOGITS, 0, tm=m, tn=n,
                                  amax_base=n, gamma=lm_gamma)
                 add_task(f"lm_head.t{m * nt + n}", -1, L.OP_GEMM, L.LEVEL_CU,
-                         None, "e.final_norm", "e.lm_head", po, n_layers)
+                         None, lm_wait, "e.lm_head", po, n_layers)
         required[ev_index["e.lm_head"]] = mt * nt
         amax_slots = nt
     p = L.ArgmaxParams()
