@@ -66,6 +66,9 @@ extern "C" {
 #define MK_EPI_SILU 2     /* fused gate/up halves: y = silu(g) * u           */
 #define MK_EPI_LOGITS 3   /* LM head: fp32 logits + per-worker argmax        */
 
+#define MK_BODY_GEMV 0   /* CUDA cores, 128-bit weight streaming (batch <= 16)  */
+#define MK_BODY_UMMA 1   /* tcgen05.mma: 128 weight rows x batch, TMEM accum.   */
+
 #define MK_TRAV_N_MAJOR 0
 #define MK_TRAV_M_MAJOR 1
 #define MK_DIST_M_TILE 0
@@ -136,6 +139,8 @@ typedef struct mk_gemm_params {
   int32_t amax_stride;/* LOGITS: rows per worker slot                       */
   int32_t stage_x;    /* 1: stage x rows in shared memory per m-tile          */
   float norm_eps;
+  int32_t body;       /* MK_BODY_*: CUDA-core warp-row GEMV or tcgen05 UMMA   */
+  int32_t y_cols;     /* valid output columns of y (masks padded LM-head rows) */
 } mk_gemm_params;
 
 typedef struct mk_norm_params {

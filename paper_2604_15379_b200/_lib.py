@@ -17,6 +17,7 @@ MK_OK, MK_ERR_CONFIG, MK_ERR_DEADLOCK, MK_ERR_CUDA = 0, 2, 3, 4
 LEVEL_WAVEFRONT, LEVEL_CU, LEVEL_CHIPLET = 0, 1, 2
 OP_NOP, OP_RMSNORM, OP_GEMM, OP_ATTN_PARTIAL, OP_ATTN_REDUCE, OP_SILU, OP_ARGMAX = range(7)
 EPI_NONE, EPI_RESIDUAL, EPI_SILU, EPI_LOGITS = range(4)
+BODY_GEMV, BODY_UMMA = 0, 1
 TRAV_N_MAJOR, TRAV_M_MAJOR = 0, 1
 DIST_M_TILE, DIST_M_SPLIT = 0, 1
 SCHED_PER_DIE, SCHED_FLAT = 0, 1
@@ -52,7 +53,7 @@ class GemmParams(C.Structure):
                 ("epilogue", I32), ("traversal", I32), ("distribution", I32),
                 ("xcd", I32), ("tile_m", I32), ("tile_n", I32),
                 ("amax_base", I32), ("amax_stride", I32), ("stage_x", I32),
-                ("norm_eps", F32)]
+                ("norm_eps", F32), ("body", I32), ("y_cols", I32)]
 
 
 class NormParams(C.Structure):

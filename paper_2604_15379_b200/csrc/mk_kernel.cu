@@ -56,6 +56,9 @@ constexpr int kSlots = 10;
 constexpr int kXsBytes = 32768;                 // staged activations per task
 constexpr int kMaxSplits = 128;                 // split-KV splits per row
 constexpr int kMaxPieces = 512;                 // splits x token subsets
+constexpr int kXStages = 4;                     // UMMA activation ring (8 KiB each)
+constexpr int kXStageBytes = 8192;              // 64 rows x 64 bf16, 128B-swizzled
+constexpr int kTmemCols = 128;                  // 2 accumulator buffers x 64 columns
 constexpr int kTQ = 32;                         // smem unit queue depth
 constexpr int kMailbox = 64;                    // mailbox depth per worker
 constexpr uint32_t kEnd = 0xFFFFFFu;
@@ -98,6 +101,7 @@ struct KArgs {
   int W;
   uint32_t epoch;
   int debug;               // bit0: consumers skip GEMM math, bit1: fetch issues no TMA
+  int use_umma;            // graph has tcgen05 GEMM tasks: allocate TMEM, run the MMA warp
 };
 
 struct AttnScratch {
@@ -118,6 +122,12 @@ struct Smem {
   float rs[kMaxNB];                 // x-staging: 1/rms per staged row
   int4 cur;                         // consumer broadcast: current unit
   int abort_flag;
+  // tcgen05 path
+  uint64_t xfull[kXStages], xempty[kXStages];
+  uint64_t tile_done[2], tmem_free[2];
+  uint64_t job_full;
+  int4 job;                         // {task, worker-in-task, first ring slot, 0}
+  uint32_t tmem_base;
   union __align__(16) {
     AttnScratch at;
     uint16_t xs[kXsBytes / 2];      // GEMM: staged (normalised) activations
@@ -725,6 +735,223 @@ __device__ void gemm_task(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
     }
   }
   bar_sync(1, kCons);   // staged rows / amx[] reusable by the next unit
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 skinny GEMM (batch >= 16): D[128 weight rows x NT batch rows] in
+// TMEM += W_tile[128 x 64] (ring slot, pre-swizzled in HBM) . X[NT x 64]^T
+// (x ring, staged + swizzled by consumer warps 0-3).  One lane of producer
+// warp 2 issues the MMAs (mma_warp), consumer warps 4-7 drain the
+// double-buffered accumulator (tcgen05.ld) into the epilogue.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int umma_nt(const mk_gemm_params& p) {
+  const int rows = min(p.T_M, p.M);
+  return (rows + 15) / 16 * 16;
+}
+
+__device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
+  uint32_t jq = 0, xs_k = 0, tb_k = 0;
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t xring_s = smem_u32(s.u.xs);
+  for (;;) {
+    if (!mbar_wait(a, &s.job_full, jq & 1, -9)) return;
+    ++jq;
+    const int4 job = s.job;
+    if (job.x < 0) return;
+    const mk_task& t = a.tasks[job.x];
+    const mk_gemm_params& p = *P<mk_gemm_params>(a, t);
+    const int NT = umma_nt(p);
+    const uint32_t idesc = umma_idesc_bf16(128, NT);
+    const int chunks = p.K / p.T_K;
+    uint32_t slot = uint32_t(job.z);
+    TileIter it;
+    it.init(p, a.W, job.y);
+    int m, n;
+    while (it.next(m, n)) {
+      const int buf = tb_k & 1;
+      if (!mbar_wait(a, &s.tmem_free[buf], ((tb_k >> 1) & 1) ^ 1, -10)) return;
+      tc_fence_after();
+      const uint32_t d = s.tmem_base + uint32_t(buf * 64);
+      for (int c = 0; c < chunks; ++c) {
+        const int i = slot % kSlots;
+        const int xi = xs_k % kXStages;
+        if (!mbar_wait(a, &s.full[i], (slot / kSlots) & 1, -11)) return;
+        if (!mbar_wait(a, &s.xfull[xi], (xs_k / kXStages) & 1, -12)) return;
+        tc_fence_after();
+        const uint32_t a_base = ring_s + uint32_t(i) * kSlotBytes;
+        const uint32_t b_base = xring_s + uint32_t(xi) * kXStageBytes;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)   // UMMA_K = 16 bf16 = 32 bytes along the swizzled row
+          umma_bf16(d, umma_desc_sw128(a_base + kk * 32), umma_desc_sw128(b_base + kk * 32),
+                    idesc, (c | kk) != 0);
+#pragma unroll
+        for (int w = 0; w < kConsWarps; ++w) umma_commit(&s.empty[i]);   // ring slot: 8 arrivals
+        umma_commit(&s.xempty[xi]);
+        ++slot; ++xs_k;
+      }
+      umma_commit(&s.tile_done[buf]);
+      ++tb_k;
+    }
+  }
+}
+
+// Consumer warps 0-3: stage the activation chunks of every tile into the
+// x ring, 128B-swizzled K-major [NT rows][64], zero rows past the batch.
+__device__ void umma_stage(const KArgs& a, Smem& s, const mk_gemm_params& p, int w_in_task,
+                           int ct, uint32_t& xs_k) {
+  const int NT = umma_nt(p);
+  const int chunks = p.K / p.T_K;
+  const uint16_t* x = reinterpret_cast<const uint16_t*>(p.x);
+  const int lane = ct & 31;
+  TileIter it;
+  it.init(p, a.W, w_in_task);
+  int m, n;
+  while (it.next(m, n)) {
+    const int m0 = m * p.T_M;
+    const int rows_m = min(p.T_M, p.M - m0);
+    for (int c = 0; c < chunks; ++c) {
+      const int xi = xs_k % kXStages;
+      mbar_wait(a, &s.xempty[xi], ((xs_k / kXStages) & 1) ^ 1, -13);
+      uint8_t* xb = reinterpret_cast<uint8_t*>(s.u.xs) + size_t(xi) * kXStageBytes;
+      for (int sg = ct; sg < NT * 8; sg += 128) {
+        const int row = sg >> 3, ch = sg & 7;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (row < rows_m) v = ldg128_cg(x + size_t(m0 + row) * p.ldx + c * 64 + ch * 8);
+        *reinterpret_cast<uint4*>(xb + row * 128 + ((ch ^ (row & 7)) << 4)) = v;
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s.xfull[xi]);
+      ++xs_k;
+    }
+  }
+}
+
+// Consumer warps 4-7 (CTA warps 8-11, TMEM lane quadrant q = warp % 4):
+// accumulator -> registers -> residual / SiLU / logits epilogue.
+__device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, int w_in_task,
+                              int ct, uint32_t& tb_k) {
+  const int NT = umma_nt(p);
+  const int lane = ct & 31;
+  const int q = (ct >> 5) & 3;
+  const int cw = ct >> 5;                 // consumer warp index (amx slot)
+  const bool silu = p.epilogue == MK_EPI_SILU;
+  TileIter it;
+  it.init(p, a.W, w_in_task);
+  int m, n;
+  while (it.next(m, n)) {
+    const int m0 = m * p.T_M;
+    const int rows_m = min(p.T_M, p.M - m0);
+    const int buf = tb_k & 1;
+    mbar_wait(a, &s.tile_done[buf], (tb_k >> 1) & 1, -14);
+    tc_fence_after();
+    const int row = 32 * q + lane;        // weight row inside the tile
+    const int out_col0 = p.y_col0 + n * p.T_N;
+    for (int j = 0; j < NT / 16; ++j) {
+      float v[16];
+      tmem_ld16(s.tmem_base + (uint32_t(32 * q) << 16) + uint32_t(buf * 64 + 16 * j), v);
+      if (p.epilogue == MK_EPI_LOGITS) {
+        float* y = reinterpret_cast<float*>(p.y);
+        const int col = out_col0 + row;
+        const bool valid_col = col < p.y_cols;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int bi = 16 * j + i;
+          float val = valid_col ? v[i] : -INFINITY;
+          if (y && valid_col && bi < rows_m) y[size_t(m0 + bi) * p.ldy + col] = val;
+          int idx = col;
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            const float v2 = __shfl_xor_sync(0xffffffffu, val, off);
+            const int i2 = __shfl_xor_sync(0xffffffffu, idx, off);
+            if (v2 > val || (v2 == val && i2 < idx)) { val = v2; idx = i2; }
+          }
+          if (lane == 0 && bi < rows_m) {
+            float& bv = s.amx_val[cw][m0 + bi];
+            int& bx = s.amx_idx[cw][m0 + bi];
+            if (val > bv || (val == bv && idx < bx)) { bv = val; bx = idx; }
+          }
+        }
+      } else if (silu) {
+        // rows 32q..32q+15 are gate rows 16q.., rows 32q+16.. the matching up rows
+        uint16_t* y = reinterpret_cast<uint16_t*>(p.y);
+        const int col = out_col0 + 16 * q + (lane & 15);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float u = __shfl_down_sync(0xffffffffu, v[i], 16);
+          const int bi = 16 * j + i;
+          if (lane < 16 && bi < rows_m)
+            y[size_t(m0 + bi) * p.ldy + col] = f2bf(v[i] / (1.f + __expf(-v[i])) * u);
+        }
+      } else {
+        uint16_t* y = reinterpret_cast<uint16_t*>(p.y);
+        const uint16_t* res = reinterpret_cast<const uint16_t*>(p.res);
+        const int col = out_col0 + row;
+        float rv[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int bi = 16 * j + i;
+          rv[i] = (p.epilogue == MK_EPI_RESIDUAL && bi < rows_m)
+                      ? bf2f(ldg16_cg(res + size_t(m0 + bi) * p.ldres + col)) : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int bi = 16 * j + i;
+          if (bi < rows_m) y[size_t(m0 + bi) * p.ldy + col] = f2bf(v[i] + rv[i]);
+        }
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s.tmem_free[buf]);
+    ++tb_k;
+  }
+}
+
+__device__ void run_gemm_umma(const KArgs& a, Smem& s, Ring& r, const mk_task& t, int tix,
+                              int worker, int ct, uint32_t& xs_k, uint32_t& tb_k,
+                              unsigned long long& tiles) {
+  const mk_gemm_params& p = *P<mk_gemm_params>(a, t);
+  const int w_in_task = t.level == MK_LEVEL_CHIPLET ? worker : 0;
+  if (p.epilogue == MK_EPI_LOGITS) {
+    for (int e = ct; e < kConsWarps * kAmaxRows; e += kCons) {
+      s.amx_val[e / kAmaxRows][e % kAmaxRows] = -INFINITY;
+      s.amx_idx[e / kAmaxRows][e % kAmaxRows] = 0x7fffffff;
+    }
+  }
+  // count the unit's ring slots and hand the job to the MMA warp
+  int n_tiles_here = 0;
+  {
+    TileIter it;
+    it.init(p, a.W, w_in_task);
+    int m, n;
+    while (it.next(m, n)) ++n_tiles_here;
+  }
+  bar_sync(1, kCons);
+  if (ct == 0) {
+    s.job = make_int4(tix, w_in_task, int(r.k), 0);
+    mbar_arrive(&s.job_full);
+  }
+  if (ct < 128) umma_stage(a, s, p, w_in_task, ct, xs_k);
+  else umma_epilogue(a, s, p, w_in_task, ct - 128 + 128, tb_k);
+  bar_sync(1, kCons);
+  r.k += uint32_t(n_tiles_here) * uint32_t(p.K / p.T_K);
+  if (ct == 0) tiles += n_tiles_here;
+  if (p.epilogue == MK_EPI_LOGITS) {
+    const int slot = p.amax_base + w_in_task;
+    for (int b = ct; b < p.M && b < kAmaxRows; b += kCons) {
+      float best = -INFINITY;
+      int bi = 0x7fffffff;
+      for (int w = 0; w < kConsWarps; ++w) {
+        const float v = s.amx_val[w][b];
+        const int i = s.amx_idx[w][b];
+        if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+      }
+      p.amax_val[size_t(slot) * p.amax_stride + b] = best;
+      p.amax_idx[size_t(slot) * p.amax_stride + b] = bi;
+    }
+    bar_sync(1, kCons);
+  }
 }
 
 __device__ void run_gemm(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
@@ -1340,6 +1567,7 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
   unsigned long long n_glob = 0, n_loc = 0, n_fence = 0, n_fan = 0, n_poll = 0, n_tiles = 0,
                      n_exec = 0;
   uint64_t t_start = 0;
+  uint32_t xs_k = 0, tb_k = 0;      // tcgen05 path: x-ring / accumulator-buffer counters
   for (;;) {
     const int qi = q % kTQ;
     // thread 0 takes the next unit and resolves its dependencies; the
@@ -1372,7 +1600,12 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
     if (ent.x < 0 || s.abort_flag) break;
     const mk_task& t = a.tasks[ent.x];
     switch (t.op) {
-      case MK_OP_GEMM: run_gemm(a, s, ring, r, t, worker, gw, ent.x, ct, n_tiles); break;
+      case MK_OP_GEMM:
+        if (P<mk_gemm_params>(a, t)->body == MK_BODY_UMMA)
+          run_gemm_umma(a, s, r, t, ent.x, worker, ct, xs_k, tb_k, n_tiles);
+        else
+          run_gemm(a, s, ring, r, t, worker, gw, ent.x, ct, n_tiles);
+        break;
       case MK_OP_RMSNORM: run_rmsnorm(a, s, t, ent.y, ent.z, ct); break;
       case MK_OP_ATTN_PARTIAL: run_attn_partial(a, s, ring, r, t, ent.y, ent.z, ct); break;
       case MK_OP_ATTN_REDUCE: run_attn_reduce(a, s, t, ent.y, ent.z, ct); break;
@@ -1410,6 +1643,10 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
     }
     ++q;
   }
+  if (ct == 0 && a.use_umma) {     // release the MMA warp
+    s.job = make_int4(-1, 0, 0, 0);
+    mbar_arrive(&s.job_full);
+  }
   if (ct == 0) {
     atomicAdd(&a.stats[S_GLOBAL], n_glob);
     atomicAdd(&a.stats[S_LOCAL], n_loc);
@@ -1435,6 +1672,9 @@ __global__ void __launch_bounds__(kThreads, 1) megakernel(const KArgs a) {
     role[1] = rank;
     for (int i = 0; i < kSlots; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], kConsWarps); }
     for (int i = 0; i < kTQ; ++i) { mbar_init(&s.tq_full[i], 1); mbar_init(&s.tq_empty[i], 1); }
+    for (int i = 0; i < kXStages; ++i) { mbar_init(&s.xfull[i], 4); mbar_init(&s.xempty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&s.tile_done[i], 1); mbar_init(&s.tmem_free[i], 4); }
+    mbar_init(&s.job_full, 1);
     fence_mbar_init();
     if (blockIdx.x == 0) atomicAdd(&a.stats[S_STEPS], 1ull);
   }
@@ -1447,12 +1687,27 @@ __global__ void __launch_bounds__(kThreads, 1) megakernel(const KArgs a) {
   }
   const int worker = rank - 1;
   if (worker >= a.W) return;             // extra SMs of the larger die idle
+  if (a.use_umma) {                      // TMEM for the tcgen05 accumulators
+    if ((threadIdx.x >> 5) == 2) {
+      tmem_alloc(&s.tmem_base, kTmemCols);
+      tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   // warp specialisation with register reallocation: the producer warpgroup
   // drops to kProdRegs, the two consumer warpgroups grow to kConsRegs
   if (threadIdx.x < kProdThreads) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(kProdRegs));
     if (threadIdx.x < 32) ring_warp(a, s, ring, worker);
     else if (threadIdx.x < 64) mailbox_warp(a, s, g, worker);
+    else if (threadIdx.x < 96 && a.use_umma) {
+      if ((threadIdx.x & 31) == 0) mma_warp(a, s, ring);
+      __syncwarp();
+      tc_fence_after();
+      tmem_dealloc(s.tmem_base, kTmemCols);
+    }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(kConsRegs));
     consumers(a, s, ring, g, worker);
@@ -1525,6 +1780,7 @@ struct mk_handle {
   uint32_t epoch = 0;
   double watchdog_s = 5.0;
   int debug = 0;
+  int use_umma = 0;
   // device buffers
   mk_task* d_tasks = nullptr;
   mk_unit* d_units = nullptr;
@@ -1719,6 +1975,13 @@ static int validate_graph(const mk_graph_desc* g) {
     if (t.op == MK_OP_GEMM) {
       const mk_gemm_params* p = reinterpret_cast<const mk_gemm_params*>(
           static_cast<const uint8_t*>(g->params) + t.param_off);
+      if (p->body == MK_BODY_UMMA) {
+        const int R = p->T_N * (p->epilogue == MK_EPI_SILU ? 2 : 1);
+        if (R != 128 || p->T_K != 64 || p->K % 64 || p->N % 128 || p->T_M > 64 || p->stage_x ||
+            p->norm_gamma || (p->epilogue == MK_EPI_LOGITS && p->M > kAmaxRows))
+          return fail(MK_ERR_CONFIG, "umma gemm task " + std::to_string(i) + " has an unsupported tile");
+        continue;
+      }
       const int R = p->T_N * (p->epilogue == MK_EPI_SILU ? 2 : 1);
       const bool kc_ok = (p->T_K % 256 == 0) || (p->T_K == p->K && p->T_K % 8 == 0 && p->T_K < 256);
       if (!kc_ok || p->K % p->T_K || size_t(R) * p->T_K * 2 > size_t(kSlotBytes) ||
@@ -1844,6 +2107,13 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
     delete h;
     return fail(MK_ERR_CONFIG, "megakernel occupancy is " + std::to_string(occ) + ", need exactly 1");
   }
+  for (int i = 0; i < g->n_tasks; ++i) {
+    const mk_task& t = g->tasks[i];
+    if (t.op == MK_OP_GEMM &&
+        reinterpret_cast<const mk_gemm_params*>(static_cast<const uint8_t*>(g->params) + t.param_off)->body ==
+            MK_BODY_UMMA)
+      h->use_umma = 1;
+  }
   rc = reset_state(h);
   if (rc) { delete h; return rc; }
   *out = h;
@@ -1868,6 +2138,7 @@ int mk_step(mk_handle* h, void* stream) {
   a.n_events = h->n_events; a.n_sched = h->n_sched; a.sched_mode = h->sched_mode; a.W = h->W;
   a.epoch = h->epoch;
   a.debug = h->debug;
+  a.use_umma = h->use_umma;
   void* args[] = {&a};
   CK(cudaLaunchCooperativeKernel((const void*)megakernel, dim3(h->num_sms), dim3(kThreads), args,
                                  kSmemBytes, static_cast<cudaStream_t>(stream)));

@@ -166,6 +166,38 @@ def pack_gate_up_fused(gate: torch.Tensor, up: torch.Tensor, dies: int,
     return both.permute(0, 1, 4, 2, 3, 5).contiguous()   # [X, nt, kc, 2, t_n, t_k]
 
 
+def swizzle128(block: torch.Tensor) -> torch.Tensor:
+    """Apply the 128-byte shared-memory swizzle to [..., rows, 64] bf16 blocks.
+
+    K-major SWIZZLE_128B (the tcgen05 / TMA layout): a row is 128 bytes = eight
+    16-byte chunks; inside every 8-row / 1024-byte atom, logical chunk c of
+    row r is stored at chunk c ^ (r % 8).  Packing the weights this way in
+    HBM lets a plain 1-D TMA bulk copy land a tile directly in the layout the
+    UMMA shared-memory descriptor expects.
+    """
+    *lead, rows, cols = block.shape
+    assert cols == 64
+    v = block.reshape(*lead, rows, 8, 8)
+    r = torch.arange(rows, device=block.device).view(rows, 1) % 8
+    phys = torch.arange(8, device=block.device).view(1, 8)
+    src = (phys ^ r)                                   # physical chunk <- logical chunk
+    idx = src.view(*([1] * len(lead)), rows, 8, 1).expand(*lead, rows, 8, 8)
+    return torch.gather(v, -2, idx).reshape(*lead, rows, cols)
+
+
+def pack_umma(w: torch.Tensor, t_n: int = 128, t_k: int = 64) -> torch.Tensor:
+    """[N, K] -> [N/t_n, K/t_k, t_n, t_k] tiles, each swizzled for tcgen05."""
+    return swizzle128(pack_tiles(w, t_n, t_k)).contiguous()
+
+
+def pack_gate_up_umma(gate: torch.Tensor, up: torch.Tensor, dies: int,
+                      t_n: int = 64, t_k: int = 64) -> torch.Tensor:
+    """Fused gate/up die slabs with UMMA tiles of [t_n gate ; t_n up] rows."""
+    fused = pack_gate_up_fused(gate, up, dies, t_n, t_k)   # [X, nt, kc, 2, t_n, t_k]
+    X, nt, kc = fused.shape[:3]
+    return swizzle128(fused.reshape(X, nt, kc, 2 * t_n, t_k)).contiguous()
+
+
 def rope_tables(head_dim: int, theta: float, t_max: int):
     """cos/sin [t_max, head_dim/2] in fp32, as Qwen3RotaryEmbedding computes
     them (modeling_qwen3.py:112-150: inv_freq = 1/theta^(2i/d), freqs = p*inv)."""

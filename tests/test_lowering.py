@@ -1,0 +1,118 @@
+"""Host graph compiler invariants (CPU only: descriptors are lowered against
+CPU tensors, nothing is launched)."""
+
+import pytest
+
+from paper_2604_15379_b200 import (Distribution, Traversal, build_decoder_layer,
+                                   model_preset, preset)
+from paper_2604_15379_b200 import _lib as L
+from paper_2604_15379_b200.analytics import device_tiles
+from paper_2604_15379_b200.lowering import LoweringOptions, lower
+from paper_2604_15379_b200.runtime import _default_lm_tile, build_state
+from paper_2604_15379_b200.weights import Qwen3Spec, Qwen3Weights
+
+W = 73
+
+
+def _lower(mode, B, fanout=True, bypass=True, layers=2, per_die=None):
+    m = model_preset("toy")
+    mach = preset("b200")
+    g = build_decoder_layer(m, mach, mode, B, tile_overrides=device_tiles(m, mach, mode, B),
+                            layers=layers)
+    spec = Qwen3Spec.toy(layers=layers)
+    w = Qwen3Weights.random(spec, seed=1)
+    per_die = (mode == "chiplet") if per_die is None else per_die
+    lm = _default_lm_tile(spec, B)
+    slots = 2 * W if per_die else spec.vocab // lm[1]
+    st = build_state(g, w, 128, lm, slots, device="cpu")
+    opts = LoweringOptions(sched_mode=L.SCHED_PER_DIE if per_die else L.SCHED_FLAT,
+                           workers=W if per_die else 147, n_dies=2, fanout=fanout,
+                           lm_tile=lm, bypass_noop=bypass)
+    return g, lower(g, spec, st, opts)
+
+
+@pytest.mark.parametrize("mode", ["chiplet", "standard"])
+@pytest.mark.parametrize("B", [1, 5, 20])
+@pytest.mark.parametrize("fanout", [True, False])
+def test_descriptors_cover_graph(mode, B, fanout):
+    g, low = _lower(mode, B, fanout=fanout)
+    tasks = [low.tasks[i] for i in range(len(low.tasks))]
+    # every graph task lowered exactly once, in graph order, + 3 head tasks
+    gidx = [t.graph_index for t in tasks if t.graph_index >= 0]
+    assert gidx == list(range(len(g.tasks)))
+    assert low.task_names[:len(g.tasks)] == [t.id for t in g.tasks]
+    assert [n.split(".")[0] for n in low.task_names[len(g.tasks):]][:1] == ["final_norm"]
+    # event required counts == number of device tasks signalling each event
+    sig = {}
+    for t in tasks:
+        sig[t.signal] = sig.get(t.signal, 0) + 1
+    for e, name in enumerate(low.event_names):
+        assert low.event_required[e] == sig.get(e, 0), name
+    # graph events keep the reference required_count
+    for e, name in enumerate(low.event_names[:len(g.events)]):
+        assert low.event_required[e] == g.events[name].required_count
+    # units: each CU task's items covered exactly once, die tasks once per die list
+    units = [low.units[i] for i in range(len(low.units))]
+    cover = {}
+    for u in units:
+        cover.setdefault(u.task, []).append((u.item_begin, u.item_end))
+    for ti, t in enumerate(tasks):
+        spans = sorted(cover[ti])
+        assert len(spans) == (1 if t.level == L.LEVEL_CHIPLET else t.n_units)
+        if t.level != L.LEVEL_CHIPLET:
+            assert spans[0][0] == 0 and spans[-1][1] == t.n_items
+            for (a, b), (c, d) in zip(spans, spans[1:]):
+                assert b == c
+        assert (t.sub_ctr >= 0) == (t.n_units > 1)
+    # scheduler lists: die tasks in their die's list
+    begin = list(low.sched_begin)
+    for s in range(low.n_sched):
+        for u in units[begin[s]:begin[s + 1]]:
+            t = tasks[u.task]
+            if t.level == L.LEVEL_CHIPLET and low.n_sched > 1:
+                assert t.die == s
+
+
+def test_fanout_off_means_one_unit_per_task():
+    g, low = _lower("chiplet", 4, fanout=False)
+    assert len(low.units) == len(low.tasks)
+
+
+def test_bypass_redirects_only_fused_norm_consumers():
+    g, on = _lower("chiplet", 1, bypass=True)
+    _, off = _lower("chiplet", 1, bypass=False)
+    ev = on.event_names
+    changed = []
+    for i in range(len(on.tasks)):
+        a, b = on.tasks[i], off.tasks[i]
+        assert a.signal == b.signal
+        if a.wait0 != b.wait0:
+            changed.append((on.task_names[i], ev[b.wait0], ev[a.wait0]))
+    # L1.qkv skips L1.rms1 (no-op), gate_up skips rms2, lm_head skips final_norm;
+    # L0.qkv still waits on L0.rms1 (embedding gather)
+    names = {c[0].rsplit(".", 1)[0] for c in changed}
+    assert "L0.qkv" not in names
+    assert {"L1.qkv", "L0.gate_up", "L1.gate_up", "lm_head"} <= names
+    for name, old, new in changed:
+        assert "rms" in old or "final_norm" in old
+
+
+def test_flat_scheduler_rejects_die_bound_graph():
+    with pytest.raises(ValueError, match="die-unaware"):
+        _lower("chiplet", 1, per_die=False)
+
+
+def test_gemm_params_die_slabs():
+    g, low = _lower("chiplet", 2, layers=1)
+    import ctypes
+    blob = low.params
+    for i in range(len(low.tasks)):
+        t = low.tasks[i]
+        if t.op != L.OP_GEMM or t.level != L.LEVEL_CHIPLET or t.graph_index < 0:
+            continue
+        p = L.GemmParams.from_buffer_copy(blob[t.param_off:t.param_off + ctypes.sizeof(L.GemmParams)])
+        gt = g.tasks[t.graph_index]
+        n_loc = gt.gemm_shape[2] // 2
+        assert p.N == n_loc and p.xcd == gt.xcd_binding
+        width = n_loc // 2 if p.epilogue == L.EPI_SILU else n_loc
+        assert p.y_col0 == gt.xcd_binding * width

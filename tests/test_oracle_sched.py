@@ -1,0 +1,58 @@
+"""Pin the sync-accounting restatement (oracle/sched_accounting.py) against
+the reference simulator's own counters (tests/golden/sim_counters.json)."""
+
+import json
+import os
+
+import pytest
+
+from oracle.cases import TILE_SPECS
+from oracle.sched_accounting import dispatch_partition, expected_counters
+from paper_2604_15379_b200 import (OpKind, build_decoder_layer, build_gemm_graph,
+                                   load_machine, model_preset, preset)
+from paper_2604_15379_b200.analytics import fit_tiles
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+SIMS = json.load(open(os.path.join(GOLD, "sim_counters.json")))
+
+
+def _machine(name):
+    if name == "b200":
+        return load_machine(os.path.join(GOLD, "b200_machine.json"))
+    return preset(name)
+
+
+def _graph(c):
+    mach = _machine(c["machine"])
+    if c["kind"] == "gemm":
+        return mach, build_gemm_graph(mach, tuple(c["shape"]), tuple(c["tiles"]),
+                                      c["mode"])
+    model = model_preset(c["model"])
+    if c["tiles"] == "fit":
+        tiles = fit_tiles(model, mach, c["mode"])
+    else:
+        raw = TILE_SPECS[c["tiles"]]
+        tiles = {(k if k == "silu_chunk" else OpKind(k)):
+                 (v if k == "silu_chunk" else tuple(v)) for k, v in raw.items()}
+    return mach, build_decoder_layer(model, mach, c["mode"], c["batch"],
+                                     tile_overrides=tiles, layers=c["layers"])
+
+
+@pytest.mark.parametrize("case", SIMS, ids=lambda c: f"{c['kind']}-{c['machine']}-{c['mode']}")
+def test_counters_match_reference_simulate(case):
+    mach, g = _graph(case)
+    exp = expected_counters(g, mach.workers_per_xcd)
+    for k in ("dispatches", "fences", "local_atomics", "global_atomics"):
+        assert exp[k] == case[k], k
+
+
+@pytest.mark.parametrize("case", [c for c in SIMS if c.get("log")],
+                         ids=lambda c: f"{c['machine']}-{c['mode']}-b{c['batch']}")
+def test_per_die_dispatch_order_matches_reference_log(case):
+    mach, g = _graph(case)
+    lists = dispatch_partition(g, mach.num_xcds)
+    per_die = [[] for _ in range(mach.num_xcds)]
+    for step, actor, action, tid in case["log"]:
+        if action == "dispatch":
+            per_die[int(actor.split(".x")[1])].append(tid)
+    assert per_die == lists
