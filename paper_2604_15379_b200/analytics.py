@@ -83,8 +83,46 @@ def fit_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
     return out
 
 
+UMMA_MIN_BATCH = 16      # batch rows from which the tcgen05 body is used
+
+
+def umma_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
+               t_m: int = 16) -> dict:
+    """Tiles of the tcgen05 body: 128 weight rows (UMMA M) x 64-wide K chunks
+    (one 128B-swizzled 16 KiB ring slot); the fused gate/up die task carries
+    64 SiLU columns (64 gate + 64 up rows) per tile."""
+    out = {}
+    for op in LINEAR_OPS:
+        fused = op is OpKind.GATE_UP_SILU and graph_mode == "chiplet"
+        out[op] = (t_m, 64 if fused else 128, 64)
+    out["silu_chunk"] = min(STANDARD_TILE_PROFILE["silu_chunk"], model.ffn_dim)
+    return out
+
+
 def device_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
-                 batch: int = 1, t_m: int = 16) -> dict:
+                 batch: int = 1, t_m: int = 16, umma: bool | None = None) -> dict:
+    """Tile overrides for the device GEMM bodies: the tcgen05 body from
+    UMMA_MIN_BATCH rows per m-tile on (when every per-task width divides its
+    128-row tiles), the CUDA-core warp-row GEMV below (see gemv_tiles)."""
+    use = umma if umma is not None else min(batch, t_m) >= UMMA_MIN_BATCH
+    if use:
+        tiles = umma_tiles(model, machine, graph_mode, t_m)
+        ok = True
+        for op in LINEAR_OPS:
+            k, n = linear_gemm_dims(op, model)
+            width = n if graph_mode == "standard" else n // machine.num_xcds
+            rows = 128 if not (op is OpKind.GATE_UP_SILU and graph_mode == "chiplet") else 128
+            if op is OpKind.GATE_UP_SILU and graph_mode == "chiplet":
+                width //= 2
+                rows = 64
+            ok = ok and width % rows == 0 and k % 64 == 0
+        if ok:
+            return tiles
+    return gemv_tiles(model, machine, graph_mode, batch, t_m)
+
+
+def gemv_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
+               batch: int = 1, t_m: int = 16) -> dict:
     """B200 tile overrides for the warp-row GEMM body (csrc gemm_tile).
 
     One shared-memory ring slot holds ``R x T_K`` bf16 (16 KiB) with

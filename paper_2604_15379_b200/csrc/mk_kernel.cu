@@ -128,7 +128,7 @@ struct Smem {
   uint64_t job_full;
   int4 job;                         // {task, worker-in-task, first ring slot, 0}
   uint32_t tmem_base;
-  union __align__(16) {
+  union __align__(1024) {            // 1024: 128B-swizzle atoms of the x ring
     AttnScratch at;
     uint16_t xs[kXsBytes / 2];      // GEMM: staged (normalised) activations
   } u;
@@ -722,7 +722,10 @@ __device__ void gemm_task(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
     }
     bar_sync(1, kCons);
     const int slot = p.amax_base + w_in_task;
-    for (int b = ct; b < p.M && b < kAmaxRows; b += kCons) {
+    // a CU tile task owns only its m-tile's rows of the shared slot
+    const int b_lo = p.tile_m >= 0 ? p.tile_m * p.T_M : 0;
+    const int b_hi = p.tile_m >= 0 ? min(p.M, b_lo + p.T_M) : p.M;
+    for (int b = b_lo + ct; b < b_hi && b < kAmaxRows; b += kCons) {
       float best = -INFINITY;
       int bi = 0x7fffffff;
       for (int w = 0; w < kConsWarps; ++w) {
@@ -939,7 +942,10 @@ __device__ void run_gemm_umma(const KArgs& a, Smem& s, Ring& r, const mk_task& t
   if (ct == 0) tiles += n_tiles_here;
   if (p.epilogue == MK_EPI_LOGITS) {
     const int slot = p.amax_base + w_in_task;
-    for (int b = ct; b < p.M && b < kAmaxRows; b += kCons) {
+    // a CU tile task owns only its m-tile's rows of the shared slot
+    const int b_lo = p.tile_m >= 0 ? p.tile_m * p.T_M : 0;
+    const int b_hi = p.tile_m >= 0 ? min(p.M, b_lo + p.T_M) : p.M;
+    for (int b = b_lo + ct; b < b_hi && b < kAmaxRows; b += kCons) {
       float best = -INFINITY;
       int bi = 0x7fffffff;
       for (int w = 0; w < kConsWarps; ++w) {

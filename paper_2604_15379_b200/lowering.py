@@ -38,6 +38,12 @@ def _cdiv(a, b):
     return (a + b - 1) // b
 
 
+def is_umma_tile(tile, fused: bool) -> bool:
+    """tcgen05 body tiles: 128 weight rows (64+64 for fused gate/up) x 64."""
+    _, t_n, t_k = tile
+    return t_k == 64 and t_n * (2 if fused else 1) == 128
+
+
 @dataclass
 class LoweringOptions:
     sched_mode: int = L.SCHED_PER_DIE
@@ -170,9 +176,12 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         return min(tile[0], M) * K * 2 <= XS_BYTES
 
     def gemm_params(w, x, y, res, M, K, N, tile, ldx, ldy, ldres, col0, epi,
-                    xcd, tm=-1, tn=-1, amax_base=0, gamma=None):
+                    xcd, tm=-1, tn=-1, amax_base=0, gamma=None, y_cols=None):
         p = L.GemmParams()
-        p.stage_x = 1 if stages(M, K, tile) else 0
+        umma = is_umma_tile(tile, epi == L.EPI_SILU)
+        p.body = L.BODY_UMMA if umma else L.BODY_GEMV
+        p.stage_x = 0 if umma else (1 if stages(M, K, tile) else 0)
+        p.y_cols = y_cols if y_cols is not None else (1 << 30)
         if gamma is not None:
             assert p.stage_x
             p.norm_gamma = _ptr(gamma)
@@ -226,10 +235,12 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                 return tuple(t.tile_shape)
         return None
 
+    gu_fused = g.mode == "chiplet"
     fuse = opts.fuse_norm and all(
-        stages(B, d, tl) for tl in (gemm_tile_of(OpKind.QKV_PROJ),
-                                    gemm_tile_of(OpKind.GATE_UP_SILU),
-                                    opts.lm_tile))
+        stages(B, d, tl) and not is_umma_tile(tl, f)
+        for tl, f in ((gemm_tile_of(OpKind.QKV_PROJ), False),
+                      (gemm_tile_of(OpKind.GATE_UP_SILU), gu_fused),
+                      (opts.lm_tile, False)))
     # attention units: at most one per worker (a second unit on a worker
     # would serialise behind the first)
     u_attn = max(1, total_workers // spec.kv_heads)
@@ -348,7 +359,7 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
     lm_wait = last_event if (fuse and opts.bypass_noop) else "e.final_norm"
     required[ev_index["e.final_norm"]] = 1
     t_m, t_n, t_k = opts.lm_tile
-    V = spec.vocab
+    V = bufs.vocab_pad or spec.vocab          # padded for 128-row tcgen05 tiles
     logits = bufs.logits
     if per_die:
         X = opts.n_dies
@@ -358,7 +369,8 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                              _ptr(lm_x), _ptr(logits), None,
                              B, d, n_loc, (t_m, t_n, t_k), d, V, d,
                              xd * n_loc, L.EPI_LOGITS, xd,
-                             amax_base=xd * opts.workers, gamma=lm_gamma)
+                             amax_base=xd * opts.workers, gamma=lm_gamma,
+                             y_cols=spec.vocab)
             add_task(f"lm_head.x{xd}", -1, L.OP_GEMM, L.LEVEL_CHIPLET, xd,
                      lm_wait, "e.lm_head", po, n_layers, n_items=0)
         required[ev_index["e.lm_head"]] = X
@@ -370,7 +382,7 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                 po = gemm_params(_ptr(bufs.lm_packed), _ptr(lm_x),
                                  _ptr(logits), None, B, d, V, (t_m, t_n, t_k),
                                  d, V, d, 0, L.EPI_LOGITS, 0, tm=m, tn=n,
-                                 amax_base=n, gamma=lm_gamma)
+                                 amax_base=n, gamma=lm_gamma, y_cols=spec.vocab)
                 add_task(f"lm_head.t{m * nt + n}", -1, L.OP_GEMM, L.LEVEL_CU,
                          None, lm_wait, "e.lm_head", po, n_layers)
         required[ev_index["e.lm_head"]] = mt * nt

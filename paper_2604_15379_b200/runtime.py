@@ -29,11 +29,13 @@ import torch
 
 from . import _lib as L
 from .lowering import LoweringOptions, lower
+from .analytics import UMMA_MIN_BATCH
 from .machine import b200_from_probe
 from .taskgraph import OpKind, TaskGraph, TaskLevel
 from .traversal import Distribution, Traversal
+from .lowering import is_umma_tile
 from .weights import (Qwen3Spec, Qwen3Weights, hash_uniform, pack_gate_up_fused,
-                      pack_tiles, rope_tables)
+                      pack_gate_up_umma, pack_tiles, pack_umma, pad_rows, rope_tables)
 
 
 def probe(device: int = 0) -> L.Topology:
@@ -112,6 +114,7 @@ class DeviceState:
     positions: torch.Tensor = None
     rope_cos: torch.Tensor = None
     rope_sin: torch.Tensor = None
+    vocab_pad: int = 0
 
 
 def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
@@ -133,17 +136,21 @@ def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
     for li in range(n_layers):
         Lw = w.layers[li]
         qkv = torch.cat((Lw["q"], Lw["k"], Lw["v"]), 0)
-        _, tn, tk = tiles[OpKind.QKV_PROJ]
-        packed = {"qkv": pack_tiles(qkv, tn, tk)}
-        _, tn, tk = tiles[OpKind.O_PROJ_RESIDUAL]
-        packed["o"] = pack_tiles(Lw["o"], tn, tk)
-        _, tn, tk = tiles[OpKind.GATE_UP_SILU]
+
+        def pk(w_, op):
+            _, tn, tk = tiles[op]
+            return pack_umma(w_, tn, tk) if is_umma_tile(tiles[op], False) else pack_tiles(w_, tn, tk)
+
+        packed = {"qkv": pk(qkv, OpKind.QKV_PROJ), "o": pk(Lw["o"], OpKind.O_PROJ_RESIDUAL),
+                  "down": pk(Lw["down"], OpKind.DOWN_PROJ_RESIDUAL)}
+        gt = tiles[OpKind.GATE_UP_SILU]
         if chiplet:
-            packed["gate_up"] = pack_gate_up_fused(Lw["gate"], Lw["up"], X, tn, tk)
+            if is_umma_tile(gt, True):
+                packed["gate_up"] = pack_gate_up_umma(Lw["gate"], Lw["up"], X, gt[2])
+            else:
+                packed["gate_up"] = pack_gate_up_fused(Lw["gate"], Lw["up"], X, gt[1], gt[2])
         else:
-            packed["gate_up"] = pack_tiles(torch.cat((Lw["gate"], Lw["up"]), 0), tn, tk)
-        _, tn, tk = tiles[OpKind.DOWN_PROJ_RESIDUAL]
-        packed["down"] = pack_tiles(Lw["down"], tn, tk)
+            packed["gate_up"] = pk(torch.cat((Lw["gate"], Lw["up"]), 0), OpKind.GATE_UP_SILU)
         st.w_packed.append(packed)
         st.w_layers.append({k: Lw[k] for k in ("q_norm", "k_norm", "in_norm", "post_norm")})
         st.layers.append({
@@ -160,12 +167,17 @@ def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
         st.v_cache.append(torch.zeros(B, sp.kv_heads, t_max, hd, **bf))
     del w.layers[:]
     _, tn, tk = lm_tile
-    st.lm_packed = pack_tiles(w.lm_head, tn, tk)
+    if is_umma_tile(lm_tile, False):
+        st.vocab_pad = -(-sp.vocab // 256) * 256          # 128-row tiles per die
+        st.lm_packed = pack_umma(pad_rows(w.lm_head, 256), tn, tk)
+    else:
+        st.vocab_pad = sp.vocab
+        st.lm_packed = pack_tiles(w.lm_head, tn, tk)
     st.embed = w.embed
     st.final_norm = w.final_norm
     st.x_in0 = torch.zeros(B, sp.hidden, **bf)
     st.final_normed = torch.zeros(B, sp.hidden, **bf)
-    st.logits = torch.zeros(B, sp.vocab, device=dev, dtype=torch.float32) \
+    st.logits = torch.zeros(B, st.vocab_pad, device=dev, dtype=torch.float32) \
         if keep_logits else None
     st.amax_val = torch.zeros(amax_slots, B, device=dev, dtype=torch.float32)
     st.amax_idx = torch.zeros(amax_slots, B, device=dev, dtype=torch.int32)
@@ -212,8 +224,9 @@ class Megakernel:
             sched_mode=L.SCHED_PER_DIE if per_die else L.SCHED_FLAT,
             traversal=traversal, distribution=distribution, workers=workers,
             n_dies=n_dies, fanout=fanout, lm_tile=lm_tile)
-        amax_slots = (n_dies * workers) if per_die else \
-            self.spec.vocab // lm_tile[1]
+        v_pad = (-(-self.spec.vocab // 256) * 256) if is_umma_tile(lm_tile, False) \
+            else self.spec.vocab
+        amax_slots = (n_dies * workers) if per_die else v_pad // lm_tile[1]
         self.state = build_state(g, weights, t_max, lm_tile, amax_slots,
                                  device=f"cuda:{device}",
                                  keep_logits=keep_logits)
@@ -262,7 +275,8 @@ class Megakernel:
         return self.state.out_tokens.clone()
 
     def logits(self):
-        return self.state.logits
+        lg = self.state.logits
+        return None if lg is None else lg[:, :self.spec.vocab]
 
     def counters(self) -> dict:
         c = L.Counters()
@@ -306,8 +320,11 @@ class Megakernel:
 
 
 def _default_lm_tile(spec: Qwen3Spec, batch: int, t_m: int = 16):
-    """LM-head tile, same rule as analytics.device_tiles (R rows x 8192/R)."""
+    """LM-head tile: the tcgen05 body (128 x 64, vocab padded to 256) from
+    UMMA_MIN_BATCH rows on, else the warp-row GEMV rule of gemv_tiles."""
     rows = min(batch, t_m)
+    if rows >= UMMA_MIN_BATCH and spec.hidden % 64 == 0:
+        return (t_m, 128, 64)
     t_n = 16 if rows <= 4 else 32
     while (spec.vocab // 2) % t_n and t_n > 8:
         t_n //= 2

@@ -191,11 +191,28 @@ def pack_umma(w: torch.Tensor, t_n: int = 128, t_k: int = 64) -> torch.Tensor:
 
 
 def pack_gate_up_umma(gate: torch.Tensor, up: torch.Tensor, dies: int,
-                      t_n: int = 64, t_k: int = 64) -> torch.Tensor:
-    """Fused gate/up die slabs with UMMA tiles of [t_n gate ; t_n up] rows."""
-    fused = pack_gate_up_fused(gate, up, dies, t_n, t_k)   # [X, nt, kc, 2, t_n, t_k]
-    X, nt, kc = fused.shape[:3]
-    return swizzle128(fused.reshape(X, nt, kc, 2 * t_n, t_k)).contiguous()
+                      t_k: int = 64) -> torch.Tensor:
+    """Fused gate/up die slabs for the tcgen05 body: a 128-row tile carries 64
+    SiLU output columns, interleaved in 16-row groups [g 16q.., u 16q..] so
+    that every 32-lane TMEM quadrant holds matching gate and up rows (the
+    epilogue pairs them with one warp shuffle)."""
+    f, k = gate.shape
+    fl = f // dies
+    if fl % 64 or k % t_k:
+        raise ValueError("gate/up slab does not tile into 64-column UMMA tiles")
+    g = gate.view(dies, fl // 64, 4, 16, k)
+    u = up.view(dies, fl // 64, 4, 16, k)
+    rows = torch.stack((g, u), dim=3).reshape(dies, fl // 64, 128, k)
+    tiles = rows.view(dies, fl // 64, 128, k // t_k, t_k).permute(0, 1, 3, 2, 4)
+    return swizzle128(tiles.contiguous()).contiguous()      # [X, nt, kc, 128, 64]
+
+
+def pad_rows(w: torch.Tensor, multiple: int) -> torch.Tensor:
+    n = w.shape[0]
+    pad = (-n) % multiple
+    if not pad:
+        return w
+    return torch.cat((w, torch.zeros(pad, *w.shape[1:], dtype=w.dtype, device=w.device)), 0)
 
 
 def rope_tables(head_dim: int, theta: float, t_max: int):

@@ -261,3 +261,45 @@ def test_watchdog_reports_deadlock(topo, machine):
     assert rc == L.MK_ERR_DEADLOCK
     assert b"watchdog" in lib.mk_last_error()
     lib.mk_destroy(h)
+
+
+def _mini(machine, mode, B, layers=2):
+    """Qwen3-shaped mini model whose widths divide the 128-row tcgen05 tiles."""
+    from paper_2604_15379_b200 import build_decoder_layer
+    from paper_2604_15379_b200.analytics import device_tiles
+    from paper_2604_15379_b200.machine import ModelConfig
+    from paper_2604_15379_b200.weights import Qwen3Spec
+    m = ModelConfig(hidden_dim=512, ffn_dim=1024, num_layers=layers, q_heads=4, kv_heads=2,
+                    dtype_bytes=2)
+    spec = Qwen3Spec(512, 1024, layers, 4, 2, 128, 1024)
+    g = build_decoder_layer(m, machine, mode, B, tile_overrides=device_tiles(m, machine, mode, B),
+                            layers=layers)
+    return g, spec
+
+
+@pytest.mark.parametrize("mode,sched", [("chiplet", "per_die"), ("standard", "flat")])
+@pytest.mark.parametrize("B,dist", [(16, "m_tile"), (32, "m_tile"), (48, "m_split"), (64, "m_tile")])
+def test_tcgen05_decode_matches_oracle(topo, machine, mode, sched, B, dist):
+    """Batch >= 16: linear layers and the LM head run on tcgen05.mma with TMEM
+    accumulators (GemmParams.body == MK_BODY_UMMA)."""
+    import ctypes
+    from paper_2604_15379_b200 import Distribution
+    from paper_2604_15379_b200 import _lib as L
+    from paper_2604_15379_b200.runtime import Megakernel
+    from paper_2604_15379_b200.weights import Qwen3Weights
+    g, spec = _mini(machine, mode, B)
+    w = Qwen3Weights.random(spec, seed=31)
+    mk = Megakernel(g, w, t_max=48, sched=sched, topo=topo,
+                    distribution=Distribution(dist), watchdog_s=5.0)
+    low = mk.lowered
+    bodies = set()
+    for i in range(len(low.tasks)):
+        t = low.tasks[i]
+        if t.op == L.OP_GEMM:
+            p = L.GemmParams.from_buffer_copy(
+                low.params[t.param_off:t.param_off + ctypes.sizeof(L.GemmParams)])
+            bodies.add(p.body)
+    assert bodies == {L.BODY_UMMA}
+    worst, ties = _decode_vs_oracle(mk, w, B, steps=6, t_max=48)
+    mk.close()
+    assert worst < RTOL
