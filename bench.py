@@ -146,13 +146,19 @@ def build(args, device):
         from dataclasses import replace
         model = replace(model, num_layers=args.layers)
     g = build_decoder_layer(model, machine, graph_mode, args.batch,
-                            tile_overrides=device_tiles(model, machine, graph_mode, args.batch),
+                            tile_overrides=device_tiles(model, machine, graph_mode, args.batch,
+                                                        t_m=args.t_m),
                             layers=model.num_layers)
     spec = Qwen3Spec.qwen3_8b(layers=model.num_layers)
     w = Qwen3Weights.random(spec, seed=0, device=f"cuda:{device}")
     t_max = CTX + 2 * (args.warmup + args.steps) + 64
+    lm_tile = None
+    if args.t_m is not None:
+        from paper_2604_15379_b200.runtime import _default_lm_tile
+        lm_tile = _default_lm_tile(spec, args.batch, args.t_m)
     mk = Megakernel(g, w, t_max=t_max, traversal=trav, distribution=distn, sched=sched,
-                    topo=topo, keep_logits=False, device=device)
+                    topo=topo, keep_logits=False, device=device, lm_tile=lm_tile,
+                    ksplit=not args.no_ksplit)
     del w
     torch.cuda.empty_cache()
     mk.fill_kv_random(CTX)
@@ -236,6 +242,8 @@ def run_ours(args):
         "data": "synthetic (hash-init bf16 weights, synthetic 1024-token bf16 KV)",
         "config": {
             "workload": f"Qwen3-8B decode, batch {B}, ctx {CTX}, {args.mode} megakernel",
+            "ksplit": not args.no_ksplit and args.mode != "standard",
+            "t_m": next(t.tile_shape[0] for t in mk.graph.tasks if t.tile_shape),
             "batch_per_gpu": B, "ctx": CTX, "layers": model.num_layers, "mode": args.mode,
             "parallelism": "replicas" if world > 1 else "single",
             "l2": "no flush: 15.1 GB of weights per step >> 126 MB L2",
@@ -364,6 +372,11 @@ def main():
                     choices=["chiplet_m_tile", "chiplet_m_split", "chiplet_n_major", "standard"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--t-m", type=int, default=None,
+                    help="batch rows per m-tile (default: 16 for the GEMV body, "
+                         "the whole batch up to 64 for tcgen05)")
+    ap.add_argument("--no-ksplit", action="store_true",
+                    help="die tasks own whole tiles per schedule() (no K-split)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

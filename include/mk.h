@@ -141,6 +141,14 @@ typedef struct mk_gemm_params {
   float norm_eps;
   int32_t body;       /* MK_BODY_*: CUDA-core warp-row GEMV or tcgen05 UMMA   */
   int32_t y_cols;     /* valid output columns of y (masks padded LM-head rows) */
+  int32_t ksplit;     /* 1: die-task K-split -- worker w owns K-chunk slots
+                         [w*S/W, (w+1)*S/W) of the traversal order
+                         (PAPER.md:569-573); 0: whole tiles per
+                         schedule() (traversal.py:125-202)             */
+  int32_t tile_ctr0;  /* K-split: first per-tile arrival sub-counter      */
+  int32_t piece_floats;/* K-split: floats per partial piece               */
+  int32_t pad2;
+  float* kpart;       /* K-split: partial pieces [W][2][piece_floats] fp32 */
 } mk_gemm_params;
 
 typedef struct mk_norm_params {

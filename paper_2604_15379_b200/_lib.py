@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmk.so")
+LIB_PATH = os.environ.get("MK_LIB_PATH") or os.path.join(_HERE, "libmk.so")
 
 MK_OK, MK_ERR_CONFIG, MK_ERR_DEADLOCK, MK_ERR_CUDA = 0, 2, 3, 4
 LEVEL_WAVEFRONT, LEVEL_CU, LEVEL_CHIPLET = 0, 1, 2
@@ -53,7 +53,9 @@ class GemmParams(C.Structure):
                 ("epilogue", I32), ("traversal", I32), ("distribution", I32),
                 ("xcd", I32), ("tile_m", I32), ("tile_n", I32),
                 ("amax_base", I32), ("amax_stride", I32), ("stage_x", I32),
-                ("norm_eps", F32), ("body", I32), ("y_cols", I32)]
+                ("norm_eps", F32), ("body", I32), ("y_cols", I32),
+                ("ksplit", I32), ("tile_ctr0", I32), ("piece_floats", I32),
+                ("pad2", I32), ("kpart", P)]
 
 
 class NormParams(C.Structure):

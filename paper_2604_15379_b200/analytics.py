@@ -84,6 +84,16 @@ def fit_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
 
 
 UMMA_MIN_BATCH = 16      # batch rows from which the tcgen05 body is used
+UMMA_MAX_TM = 64         # batch rows per tcgen05 m-tile (UMMA N, TMEM columns)
+
+
+def default_t_m(batch: int) -> int:
+    """Batch rows per m-tile: 16 for the CUDA-core GEMV (register budget),
+    the whole batch (up to 64, padded to 16) for the tcgen05 body so every
+    weight tile is streamed from HBM once per step."""
+    if batch >= UMMA_MIN_BATCH:
+        return min(UMMA_MAX_TM, -(-batch // 16) * 16)
+    return 16
 
 
 def umma_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
@@ -100,10 +110,12 @@ def umma_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
 
 
 def device_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
-                 batch: int = 1, t_m: int = 16, umma: bool | None = None) -> dict:
+                 batch: int = 1, t_m: int | None = None, umma: bool | None = None) -> dict:
     """Tile overrides for the device GEMM bodies: the tcgen05 body from
     UMMA_MIN_BATCH rows per m-tile on (when every per-task width divides its
     128-row tiles), the CUDA-core warp-row GEMV below (see gemv_tiles)."""
+    if t_m is None:
+        t_m = default_t_m(batch)
     use = umma if umma is not None else min(batch, t_m) >= UMMA_MIN_BATCH
     if use:
         tiles = umma_tiles(model, machine, graph_mode, t_m)
@@ -118,7 +130,7 @@ def device_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
             ok = ok and width % rows == 0 and k % 64 == 0
         if ok:
             return tiles
-    return gemv_tiles(model, machine, graph_mode, batch, t_m)
+    return gemv_tiles(model, machine, graph_mode, batch, min(t_m, 16))
 
 
 def gemv_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,

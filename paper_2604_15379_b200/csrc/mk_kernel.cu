@@ -39,6 +39,7 @@
 #include <vector>
 #include <string>
 #include <algorithm>
+#include <type_traits>
 
 #include "mk.h"
 #include "mk_ptx.cuh"
@@ -63,6 +64,11 @@ constexpr int kTQ = 32;                         // smem unit queue depth
 constexpr int kMailbox = 64;                    // mailbox depth per worker
 constexpr uint32_t kEnd = 0xFFFFFFu;
 constexpr int kMaxNB = 16;
+// Kernel instances: feature bits select the op bodies compiled into one
+// instance, so a small-batch graph runs a kernel without the tcgen05 and
+// K-split code (smaller code, same register allocation as the plain GEMV).
+constexpr int kFeatUmma = 1;      // tcgen05 GEMM body, MMA warp, TMEM
+constexpr int kFeatKsplit = 2;    // K-split die tasks (partial pieces)
 constexpr int kAmaxRows = 64;
 
 enum StatIdx {
@@ -122,6 +128,8 @@ struct Smem {
   float rs[kMaxNB];                 // x-staging: 1/rms per staged row
   int4 cur;                         // consumer broadcast: current unit
   int abort_flag;
+  int piece_last;                   // K-split: this CTA summed the tile's pieces (GEMV)
+  int epi_last;                     // K-split: same, tcgen05 epilogue warps
   // tcgen05 path
   uint64_t xfull[kXStages], xempty[kXStages];
   uint64_t tile_done[2], tmem_free[2];
@@ -186,7 +194,7 @@ __device__ __forceinline__ const T* P(const KArgs& a, const mk_task& t) {
 struct TileIter {
   int mt, nt, W, w, trav, dist, xcd;
   int idx, row, n, fixed_m, fixed_n, done;
-  __device__ void init(const mk_gemm_params& p, int workers, int worker) {
+  __device__ __forceinline__ void init(const mk_gemm_params& p, int workers, int worker) {
     const int rows_per_out = (p.epilogue == MK_EPI_SILU) ? 2 : 1;
     mt = (p.M + p.T_M - 1) / p.T_M;
     nt = p.N / (p.T_N * rows_per_out);
@@ -194,7 +202,7 @@ struct TileIter {
     xcd = p.xcd; fixed_m = p.tile_m; fixed_n = p.tile_n; done = 0;
     idx = w; row = 0; n = w;
   }
-  __device__ bool next(int& m_out, int& n_out) {
+  __device__ __forceinline__ bool next(int& m_out, int& n_out) {
     if (fixed_m >= 0) {              // standard-mode CU tile task
       if (done) return false;
       done = 1; m_out = fixed_m; n_out = fixed_n; return true;
@@ -221,6 +229,109 @@ __device__ __forceinline__ int gemm_rows(const mk_gemm_params& p) {
 }
 
 // ---------------------------------------------------------------------------
+// K-split range partition of a die task ("K-split", done on
+// B200 across the die's worker CTAs).  The traversal's tile order (the same
+// (m, n) sequence schedule() walks, traversal.py:125-202) is refined into its
+// K-chunks -- one 16 KiB ring slot each -- and worker w owns the contiguous
+// slot range [w*S/W, (w+1)*S/W).  Every worker streams the same number of
+// weight bytes whatever the tile count; consecutive workers still share
+// weight columns in M-major order.  A tile cut by a range boundary is
+// computed as partial pieces (fp32, per worker) and the last-arriving piece
+// sums them in piece order (deterministic) and runs the epilogue.
+// ---------------------------------------------------------------------------
+struct Seg {
+  int tile, m, n, c0, c1;
+  bool first;          // the worker's first segment (its piece slot 0)
+};
+
+__device__ __forceinline__ void tile_mn(const mk_gemm_params& p, int mt, int nt, int idx,
+                                        int& m, int& n) {
+  if (p.distribution == MK_DIST_M_SPLIT) { m = (p.xcd % mt + idx / nt) % mt; n = idx % nt; }
+  else if (p.traversal == MK_TRAV_M_MAJOR) { m = idx % mt; n = idx / mt; }
+  else { m = idx / nt; n = idx % nt; }
+}
+
+struct RangeIter {
+  int mt, nt, chunks;
+  long long s0, s1, s;
+  const mk_gemm_params* p;
+  __device__ __forceinline__ void init(const mk_gemm_params& pp, int W, int w) {
+    p = &pp;
+    mt = (pp.M + pp.T_M - 1) / pp.T_M;
+    nt = pp.N / gemm_rows(pp);
+    chunks = pp.K / pp.T_K;
+    const long long S = (long long)mt * nt * chunks;
+    s0 = S * w / W; s1 = S * (w + 1) / W; s = s0;
+  }
+  __device__ __forceinline__ bool next(Seg& g) {
+    if (s >= s1) return false;
+    g.tile = int(s / chunks);
+    g.c0 = int(s % chunks);
+    g.c1 = int(min((long long)chunks, g.c0 + (s1 - s)));
+    g.first = s == s0;
+    tile_mn(*p, mt, nt, g.tile, g.m, g.n);
+    s += g.c1 - g.c0;
+    return true;
+  }
+  __device__ long long slots() const { return s1 - s0; }
+};
+
+// Uniform segment walk: K-split ranges, or the reference's whole-tile
+// ownership (TileIter) as single full-K segments.
+struct SegIter {
+  bool ks;
+  RangeIter ri;
+  TileIter ti;
+  int chunks;
+  __device__ __forceinline__ void init(const mk_gemm_params& p, int W, int w) {
+    ks = p.ksplit != 0;
+    chunks = p.K / p.T_K;
+    if (ks) ri.init(p, W, w); else ti.init(p, W, w);
+  }
+  __device__ __forceinline__ bool next(Seg& g) {
+    if (ks) return ri.next(g);
+    if (!ti.next(g.m, g.n)) return false;
+    g.tile = -1; g.c0 = 0; g.c1 = chunks; g.first = true;
+    return true;
+  }
+};
+
+// Which worker owns slot s (inverse of w*S/W).
+__device__ __forceinline__ int range_owner(long long s, long long S, int W) {
+  return int(((s + 1) * W + S - 1) / S) - 1;
+}
+
+// The pieces of a cut tile: the non-empty worker ranges between the owners
+// of its first and last slot (with more workers than slots some ranges in
+// between are empty and contribute nothing).
+struct PieceInfo {
+  int first_w, last_w, n, slot0;   // owners, piece count, piece-slot of first_w
+  long long S;
+  int W;
+  __device__ __forceinline__ bool empty(int w) const {
+    return S * w / W == S * (w + 1) / W;
+  }
+};
+
+__device__ __forceinline__ PieceInfo tile_pieces(const mk_gemm_params& p, int W, int tile) {
+  const int mt = (p.M + p.T_M - 1) / p.T_M, nt = p.N / gemm_rows(p), chunks = p.K / p.T_K;
+  PieceInfo pi;
+  pi.S = (long long)mt * nt * chunks;
+  pi.W = W;
+  const long long a = (long long)tile * chunks, b = a + chunks - 1;
+  pi.first_w = range_owner(a, pi.S, W);
+  pi.last_w = range_owner(b, pi.S, W);
+  pi.n = 0;
+  for (int w = pi.first_w; w <= pi.last_w; ++w) pi.n += pi.empty(w) ? 0 : 1;
+  pi.slot0 = (pi.S * pi.first_w / W) < a ? 1 : 0;   // tile is not its first segment
+  return pi;
+}
+
+__device__ __forceinline__ float* piece_ptr(const mk_gemm_params& p, int worker, int slot) {
+  return p.kpart + (size_t(worker) * 2 + slot) * p.piece_floats;
+}
+
+// ---------------------------------------------------------------------------
 // Fetch warp: stream the unit's immutable operands into the ring.
 // ---------------------------------------------------------------------------
 struct Ring {
@@ -231,26 +342,27 @@ struct Ring {
 // GEMM every K-chunk of every tile this worker owns; for an attention unit
 // the cached K and V block of every item.  Walked twice by the fetch warp:
 // once to prefetch into L2, once to copy into the shared-memory ring.
+template <int F>
 struct SlotIter {
   const mk_task* t;
   int op, worker, ib, ie;
   // gemm
-  TileIter it;
+  typename std::conditional<(F & kFeatKsplit) != 0, SegIter, TileIter>::type it;
   const __nv_bfloat16* w;
-  int chunks, R, tk, c, cur_n;
+  int chunks, R, tk, c, c_end, cur_n;
   // attention
   int item, kv;                 // kv: 0 = K next, 1 = V next
   const __nv_bfloat16* src_k;
   uint32_t bytes_kv;
   bool active;
 
-  __device__ void init(const KArgs& a, const mk_task& task, int ib_, int ie_, int worker_) {
+  __device__ __forceinline__ void init(const KArgs& a, const mk_task& task, int ib_, int ie_, int worker_) {
     t = &task; op = task.op; worker = worker_; ib = ib_; ie = ie_; active = true;
     if (op == MK_OP_GEMM) {
       const mk_gemm_params& p = *reinterpret_cast<const mk_gemm_params*>(a.params + task.param_off);
       it.init(p, a.W, task.level == MK_LEVEL_CHIPLET ? worker : 0);
       w = reinterpret_cast<const __nv_bfloat16*>(p.w);
-      R = gemm_rows(p); tk = p.T_K; chunks = p.K / p.T_K; c = chunks; cur_n = 0;
+      R = gemm_rows(p); tk = p.T_K; chunks = p.K / p.T_K; c = c_end = 0; cur_n = 0;
     } else if (op == MK_OP_ATTN_PARTIAL) {
       item = ib; kv = 0; bytes_kv = 0; src_k = nullptr;
     } else {
@@ -258,13 +370,19 @@ struct SlotIter {
     }
   }
   // next slot: (src, bytes); false when the unit has no more slots
-  __device__ bool next(const KArgs& a, const void*& src, uint32_t& bytes) {
+  __device__ __forceinline__ bool next(const KArgs& a, const void*& src, uint32_t& bytes) {
     if (!active) return false;
     if (op == MK_OP_GEMM) {
-      if (c >= chunks) {
-        int m, n;
-        if (!it.next(m, n)) { active = false; return false; }
-        cur_n = n; c = 0;
+      if (c >= c_end) {
+        if constexpr ((F & kFeatKsplit) != 0) {
+          Seg g;
+          if (!it.next(g)) { active = false; return false; }
+          cur_n = g.n; c = g.c0; c_end = g.c1;
+        } else {
+          int m, n;
+          if (!it.next(m, n)) { active = false; return false; }
+          cur_n = n; c = 0; c_end = chunks;
+        }
       }
       src = w + (size_t(cur_n) * chunks + c) * R * tk;
       bytes = uint32_t(R) * tk * 2;
@@ -407,6 +525,53 @@ __device__ void stage_x(Smem& s, const mk_gemm_params& p, int m0, int rows, int 
     }
   }
   bar_sync(1, kCons);
+}
+
+// K-split piece handling for the CUDA-core body.  Called by all consumer
+// threads after the warp reduction (every lane holds tot[j][b] of rows
+// warp + 8j).  Returns true when this CTA runs the epilogue: the tile was
+// whole, or this was its last piece -- then tot holds the piece sum (lane b,
+// batch row b), summed in piece order so the result does not depend on
+// arrival order.
+template <int NB, int RPW>
+__device__ __forceinline__ bool gemv_piece(const KArgs& a, Smem& s, const mk_gemm_params& p, const Seg& g,
+                           int worker, int rows_m, int rpw, int ct, float (&tot)[RPW][NB]) {
+  if (g.c0 == 0 && g.c1 == p.K / p.T_K) return true;
+  const int warp = ct >> 5, lane = ct & 31;
+  float* mine = piece_ptr(p, worker, g.first ? 0 : 1);
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    if (lane != b || b >= rows_m) continue;
+#pragma unroll
+    for (int j = 0; j < RPW; ++j)
+      if (j < rpw) __stcg(mine + (warp + kConsWarps * j) * p.T_M + b, tot[j][b]);
+  }
+  const PieceInfo pi = tile_pieces(p, a.W, g.tile);
+  __threadfence();
+  bar_sync(1, kCons);
+  if (ct == 0) {
+    const uint32_t old = atom_acq_rel_add(&a.sub_ctr[p.tile_ctr0 + g.tile], 1u);
+    s.piece_last = (old + 1 == uint32_t(pi.n) * a.epoch) ? 1 : 0;
+  }
+  bar_sync(1, kCons);
+  if (!s.piece_last) return false;
+  __threadfence();
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    if (lane != b || b >= rows_m) continue;
+#pragma unroll
+    for (int j = 0; j < RPW; ++j) {
+      if (j >= rpw) continue;
+      float v = 0.f;
+      for (int w = pi.first_w; w <= pi.last_w; ++w) {
+        if (pi.empty(w)) continue;
+        v += __ldcg(piece_ptr(p, w, w == pi.first_w ? pi.slot0 : 0) +
+                    (warp + kConsWarps * j) * p.T_M + b);
+      }
+      tot[j][b] = v;
+    }
+  }
+  return true;
 }
 
 // Warp-owned rows: slot [R rows][KC] bf16, warp w owns rows w, w+8, w+16,
@@ -657,6 +822,140 @@ __device__ void gemm_tile_fast(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   }
 }
 
+// K-split variant of the fast path: K-chunks [c0, c1) of the tile, partial
+// pieces summed by the last piece (gemv_piece).  Rows per warp RPW in {1,2,4}, K-chunk KC = 1024/RPW (so one
+// slot = 8*RPW rows x KC = 16 KiB and every lane covers NP = 4/RPW 16-byte
+// segments per row).  All slot loads are issued before any math, the slot is
+// released as soon as the weights sit in registers, and independent
+// accumulator chains keep the FMA pipe busy.
+template <int NB, int RPW, bool XS>
+__device__ __forceinline__ void gemm_tile_fast_ks(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
+                                  const mk_gemm_params& p, const Seg& sg, int worker, int ct,
+                                  float (&amv)[NB], int (&ami)[NB]) {
+  const int m = sg.m, n = sg.n, c_begin = sg.c0, c_end = sg.c1;
+  Ring rl = r;                             // keep the ring cursor in a register
+  constexpr int NP = 4 / RPW;
+  constexpr int KC = 256 * NP;
+  constexpr int CH = (RPW * NB >= 4) ? 1 : NP;   // extra chains when few (row, b) pairs
+  const int warp = ct >> 5, lane = ct & 31;
+  const int chunks = p.K / KC;
+  const int m0 = m * p.T_M;
+  const int rows_m = min(p.T_M, p.M - m0);
+  const int out_col0 = p.y_col0 + n * p.T_N;
+  const __nv_bfloat16* x = reinterpret_cast<const __nv_bfloat16*>(p.x);
+
+  float resv[RPW];
+#pragma unroll
+  for (int j = 0; j < RPW; ++j) resv[j] = 0.f;
+  if (p.epilogue == MK_EPI_RESIDUAL && lane < rows_m) {
+    const uint16_t* res = reinterpret_cast<const uint16_t*>(p.res) + size_t(m0 + lane) * p.ldres;
+#pragma unroll
+    for (int j = 0; j < RPW; ++j) resv[j] = bf2f(ldg16_cg(res + out_col0 + warp + kConsWarps * j));
+  }
+
+  float acc[CH][RPW][NB];
+#pragma unroll
+  for (int q = 0; q < CH; ++q)
+#pragma unroll
+    for (int j = 0; j < RPW; ++j)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) acc[q][j][b] = 0.f;
+
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t xs_s = smem_u32(s.u.xs);
+  (void)chunks;
+  for (int c = c_begin; c < c_end; ++c) {
+    cons_wait_slot(a, s, rl);
+    const uint32_t slot = ring_s + uint32_t(rl.k % kSlots) * kSlotBytes;
+    uint4 wv[NP][RPW];
+#pragma unroll
+    for (int ps = 0; ps < NP; ++ps)
+#pragma unroll
+      for (int j = 0; j < RPW; ++j)
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(wv[ps][j].x), "=r"(wv[ps][j].y), "=r"(wv[ps][j].z), "=r"(wv[ps][j].w)
+                     : "r"(slot + uint32_t(((warp + kConsWarps * j) * KC + ps * 256 + lane * 8) * 2)));
+    uint4 xv[NP][NB];
+#pragma unroll
+    for (int ps = 0; ps < NP; ++ps)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int kg = c * KC + ps * 256 + lane * 8;
+        if constexpr (XS) {
+          if (b < rows_m)
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(xv[ps][b].x), "=r"(xv[ps][b].y), "=r"(xv[ps][b].z), "=r"(xv[ps][b].w)
+                         : "r"(xs_s + uint32_t((b * p.K + kg) * 2)));
+          else xv[ps][b] = make_uint4(0, 0, 0, 0);
+        } else {
+          xv[ps][b] = (b < rows_m) ? ldg128_cg(x + size_t(m0 + b) * p.ldx + kg) : make_uint4(0, 0, 0, 0);
+        }
+      }
+    cons_release_slot(s, rl);         // weights now live in registers
+    if (a.debug & 1) continue;
+#pragma unroll
+    for (int ps = 0; ps < NP; ++ps) {
+      float wf[RPW][8];
+#pragma unroll
+      for (int j = 0; j < RPW; ++j) unpack8(wv[ps][j], wf[j]);
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        float xf[8];
+        unpack8(xv[ps][b], xf);
+#pragma unroll
+        for (int j = 0; j < RPW; ++j) {
+          float& t = acc[CH == 1 ? 0 : ps][j][b];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) t = fmaf(wf[j][e], xf[e], t);
+        }
+      }
+    }
+  }
+
+  r = rl;
+  float tot[RPW][NB];
+#pragma unroll
+  for (int j = 0; j < RPW; ++j)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      float v = acc[0][j][b];
+#pragma unroll
+      for (int q = 1; q < CH; ++q) v += acc[q][j][b];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      tot[j][b] = v;
+    }
+  if (!gemv_piece<NB, RPW>(a, s, p, sg, worker, rows_m, RPW, ct, tot)) return;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    if (lane != b || b >= rows_m) continue;
+    if (p.epilogue == MK_EPI_LOGITS) {
+      float* y = reinterpret_cast<float*>(p.y);
+#pragma unroll
+      for (int j = 0; j < RPW; ++j) {
+        const int col = out_col0 + warp + kConsWarps * j;
+        const float v = tot[j][b];
+        if (y) y[size_t(m0 + b) * p.ldy + col] = v;
+        if (v > amv[b] || (v == amv[b] && col < ami[b])) { amv[b] = v; ami[b] = col; }
+      }
+    } else {
+      uint16_t* y = reinterpret_cast<uint16_t*>(p.y) + size_t(m0 + b) * p.ldy;
+      if (p.epilogue == MK_EPI_SILU) {
+        if constexpr (RPW >= 2) {
+#pragma unroll
+          for (int j = 0; j < RPW / 2; ++j) {
+            const float g = tot[j][b], u = tot[j + RPW / 2][b];
+            y[out_col0 + warp + kConsWarps * j] = f2bf(g / (1.f + __expf(-g)) * u);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < RPW; ++j) y[out_col0 + warp + kConsWarps * j] = f2bf(tot[j][b] + resv[j]);
+      }
+    }
+  }
+}
+
 template <int NB, bool XS>
 __device__ void gemm_task(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
                           const mk_gemm_params& p, int w_in_task, int gw, int tix, int ct,
@@ -740,6 +1039,93 @@ __device__ void gemm_task(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   bar_sync(1, kCons);   // staged rows / amx[] reusable by the next unit
 }
 
+// K-split die task (lowering only K-splits the fast-path shapes).
+template <int NB, bool XS>
+__device__ void gemm_task_ks(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
+                          const mk_gemm_params& p, int w_in_task, int gw, int tix, int ct,
+                          unsigned long long& tiles) {
+  const int warp = ct >> 5, lane = ct & 31;
+  float amv[NB];
+  int ami[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) { amv[b] = -INFINITY; ami[b] = 0x7fffffff; }
+  int staged_m = -1;
+  int cur_m = -1;
+  RangeIter rit;
+  rit.init(p, a.W, w_in_task);
+  int m, n;
+  Seg sg;
+  for (;;) {
+    if (!rit.next(sg)) break;
+    m = sg.m; n = sg.n;
+    if (p.epilogue == MK_EPI_LOGITS && m != cur_m) {
+      // switch the lanes' running argmax to the rows of the new m-tile
+      // (lane b always owns row m0 + b, so no cross-lane hazard)
+      const int mo = cur_m * p.T_M, mn = m * p.T_M;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        if (lane != b) continue;
+        if (cur_m >= 0 && mo + b < p.M) { s.amx_val[warp][mo + b] = amv[b]; s.amx_idx[warp][mo + b] = ami[b]; }
+        if (mn + b < p.M) { amv[b] = s.amx_val[warp][mn + b]; ami[b] = s.amx_idx[warp][mn + b]; }
+      }
+    }
+    cur_m = m;
+    if constexpr (XS) {
+      if (m != staged_m) {
+        stage_x(s, p, m * p.T_M, min(p.T_M, p.M - m * p.T_M), ct);
+        staged_m = m;
+      }
+    }
+    // fast path for the register-feasible (rows-per-warp, batch) pairs
+    const int R = gemm_rows(p);
+    bool done = false;
+    if constexpr (NB == 1) {
+      if (R == 8 && p.T_K == 1024) { gemm_tile_fast_ks<NB, 1, XS>(a, s, ring, r, p, sg, w_in_task, ct, amv, ami); done = true; }
+    }
+    if constexpr (NB <= 4) {
+      if (!done && R == 16 && p.T_K == 512) { gemm_tile_fast_ks<NB, 2, XS>(a, s, ring, r, p, sg, w_in_task, ct, amv, ami); done = true; }
+    }
+    if constexpr (NB <= 8) {
+      if (!done && R == 32 && p.T_K == 256) { gemm_tile_fast_ks<NB, 4, XS>(a, s, ring, r, p, sg, w_in_task, ct, amv, ami); done = true; }
+    }
+    if (ct == 0) {
+      ++tiles;
+      if (a.tile_log) {
+        unsigned long long at = atomicAdd(a.tile_cursor, 1ull);
+        if ((long long)at < a.tile_cap) {
+          int32_t* rec = a.tile_log + at * 4;
+          rec[0] = tix; rec[1] = gw; rec[2] = m; rec[3] = n;
+        }
+      }
+    }
+  }
+  if (p.epilogue == MK_EPI_LOGITS) {
+    if (cur_m >= 0) {
+      const int m0 = cur_m * p.T_M;
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        if (lane == b && m0 + b < p.M) { s.amx_val[warp][m0 + b] = amv[b]; s.amx_idx[warp][m0 + b] = ami[b]; }
+    }
+    bar_sync(1, kCons);
+    const int slot = p.amax_base + w_in_task;
+    // a CU tile task owns only its m-tile's rows of the shared slot
+    const int b_lo = p.tile_m >= 0 ? p.tile_m * p.T_M : 0;
+    const int b_hi = p.tile_m >= 0 ? min(p.M, b_lo + p.T_M) : p.M;
+    for (int b = b_lo + ct; b < b_hi && b < kAmaxRows; b += kCons) {
+      float best = -INFINITY;
+      int bi = 0x7fffffff;
+      for (int w = 0; w < kConsWarps; ++w) {
+        const float v = s.amx_val[w][b];
+        const int i = s.amx_idx[w][b];
+        if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+      }
+      p.amax_val[size_t(slot) * p.amax_stride + b] = best;
+      p.amax_idx[size_t(slot) * p.amax_stride + b] = bi;
+    }
+  }
+  bar_sync(1, kCons);   // staged rows / amx[] reusable by the next unit
+}
+
 // ---------------------------------------------------------------------------
 // tcgen05 skinny GEMM (batch >= 16): D[128 weight rows x NT batch rows] in
 // TMEM += W_tile[128 x 64] (ring slot, pre-swizzled in HBM) . X[NT x 64]^T
@@ -765,17 +1151,16 @@ __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
     const mk_gemm_params& p = *P<mk_gemm_params>(a, t);
     const int NT = umma_nt(p);
     const uint32_t idesc = umma_idesc_bf16(128, NT);
-    const int chunks = p.K / p.T_K;
     uint32_t slot = uint32_t(job.z);
-    TileIter it;
+    SegIter it;
     it.init(p, a.W, job.y);
-    int m, n;
-    while (it.next(m, n)) {
+    Seg sg;
+    while (it.next(sg)) {
       const int buf = tb_k & 1;
       if (!mbar_wait(a, &s.tmem_free[buf], ((tb_k >> 1) & 1) ^ 1, -10)) return;
       tc_fence_after();
       const uint32_t d = s.tmem_base + uint32_t(buf * 64);
-      for (int c = 0; c < chunks; ++c) {
+      for (int c = sg.c0; c < sg.c1; ++c) {
         const int i = slot % kSlots;
         const int xi = xs_k % kXStages;
         if (!mbar_wait(a, &s.full[i], (slot / kSlots) & 1, -11)) return;
@@ -786,7 +1171,7 @@ __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)   // UMMA_K = 16 bf16 = 32 bytes along the swizzled row
           umma_bf16(d, umma_desc_sw128(a_base + kk * 32), umma_desc_sw128(b_base + kk * 32),
-                    idesc, (c | kk) != 0);
+                    idesc, (c != sg.c0 || kk != 0));
 #pragma unroll
         for (int w = 0; w < kConsWarps; ++w) umma_commit(&s.empty[i]);   // ring slot: 8 arrivals
         umma_commit(&s.xempty[xi]);
@@ -798,21 +1183,20 @@ __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
   }
 }
 
-// Consumer warps 0-3: stage the activation chunks of every tile into the
+// Consumer warps 0-3: stage the activation chunks of every segment into the
 // x ring, 128B-swizzled K-major [NT rows][64], zero rows past the batch.
 __device__ void umma_stage(const KArgs& a, Smem& s, const mk_gemm_params& p, int w_in_task,
                            int ct, uint32_t& xs_k) {
   const int NT = umma_nt(p);
-  const int chunks = p.K / p.T_K;
   const uint16_t* x = reinterpret_cast<const uint16_t*>(p.x);
   const int lane = ct & 31;
-  TileIter it;
+  SegIter it;
   it.init(p, a.W, w_in_task);
-  int m, n;
-  while (it.next(m, n)) {
-    const int m0 = m * p.T_M;
+  Seg g;
+  while (it.next(g)) {
+    const int m0 = g.m * p.T_M;
     const int rows_m = min(p.T_M, p.M - m0);
-    for (int c = 0; c < chunks; ++c) {
+    for (int c = g.c0; c < g.c1; ++c) {
       const int xi = xs_k % kXStages;
       mbar_wait(a, &s.xempty[xi], ((xs_k / kXStages) & 1) ^ 1, -13);
       uint8_t* xb = reinterpret_cast<uint8_t*>(s.u.xs) + size_t(xi) * kXStageBytes;
@@ -830,84 +1214,137 @@ __device__ void umma_stage(const KArgs& a, Smem& s, const mk_gemm_params& p, int
   }
 }
 
+// Epilogue of 16 accumulator columns (batch rows 16j..16j+15) of weight row
+// `row` (TMEM lane): residual / interleaved SiLU / logits + running argmax.
+__device__ __forceinline__ void umma_epi16(Smem& s, const mk_gemm_params& p, int m0, int rows_m,
+                                           int out_col0, int row, int q, int lane, int cw, int j,
+                                           const float (&v)[16]) {
+  if (p.epilogue == MK_EPI_LOGITS) {
+    float* y = reinterpret_cast<float*>(p.y);
+    const int col = out_col0 + row;
+    const bool valid_col = col < p.y_cols;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int bi = 16 * j + i;
+      float val = valid_col ? v[i] : -INFINITY;
+      if (y && valid_col && bi < rows_m) y[size_t(m0 + bi) * p.ldy + col] = val;
+      int idx = col;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const float v2 = __shfl_xor_sync(0xffffffffu, val, off);
+        const int i2 = __shfl_xor_sync(0xffffffffu, idx, off);
+        if (v2 > val || (v2 == val && i2 < idx)) { val = v2; idx = i2; }
+      }
+      if (lane == 0 && bi < rows_m) {
+        float& bv = s.amx_val[cw][m0 + bi];
+        int& bx = s.amx_idx[cw][m0 + bi];
+        if (val > bv || (val == bv && idx < bx)) { bv = val; bx = idx; }
+      }
+    }
+  } else if (p.epilogue == MK_EPI_SILU) {
+    // rows 32q..32q+15 are gate rows 16q.., rows 32q+16.. the matching up rows
+    uint16_t* y = reinterpret_cast<uint16_t*>(p.y);
+    const int col = out_col0 + 16 * q + (lane & 15);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float u = __shfl_down_sync(0xffffffffu, v[i], 16);
+      const int bi = 16 * j + i;
+      if (lane < 16 && bi < rows_m)
+        y[size_t(m0 + bi) * p.ldy + col] = f2bf(v[i] / (1.f + __expf(-v[i])) * u);
+    }
+  } else {
+    uint16_t* y = reinterpret_cast<uint16_t*>(p.y);
+    const uint16_t* res = reinterpret_cast<const uint16_t*>(p.res);
+    const int col = out_col0 + row;
+    float rv[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int bi = 16 * j + i;
+      rv[i] = (p.epilogue == MK_EPI_RESIDUAL && bi < rows_m)
+                  ? bf2f(ldg16_cg(res + size_t(m0 + bi) * p.ldres + col)) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int bi = 16 * j + i;
+      if (bi < rows_m) y[size_t(m0 + bi) * p.ldy + col] = f2bf(v[i] + rv[i]);
+    }
+  }
+}
+
 // Consumer warps 4-7 (CTA warps 8-11, TMEM lane quadrant q = warp % 4):
-// accumulator -> registers -> residual / SiLU / logits epilogue.
+// accumulator -> registers -> epilogue.  A K-split piece goes to the
+// worker's piece slot ([col][128 rows] fp32, coalesced); the last piece of a
+// tile sums all pieces in piece order and runs the epilogue.
 __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, int w_in_task,
                               int ct, uint32_t& tb_k) {
   const int NT = umma_nt(p);
   const int lane = ct & 31;
   const int q = (ct >> 5) & 3;
   const int cw = ct >> 5;                 // consumer warp index (amx slot)
-  const bool silu = p.epilogue == MK_EPI_SILU;
-  TileIter it;
+  const int et = ct - 128;                // epilogue-group thread 0..127
+  const int chunks = p.K / p.T_K;
+  SegIter it;
   it.init(p, a.W, w_in_task);
-  int m, n;
-  while (it.next(m, n)) {
-    const int m0 = m * p.T_M;
+  Seg g;
+  while (it.next(g)) {
+    const int m0 = g.m * p.T_M;
     const int rows_m = min(p.T_M, p.M - m0);
     const int buf = tb_k & 1;
     mbar_wait(a, &s.tile_done[buf], (tb_k >> 1) & 1, -14);
     tc_fence_after();
     const int row = 32 * q + lane;        // weight row inside the tile
-    const int out_col0 = p.y_col0 + n * p.T_N;
+    const int out_col0 = p.y_col0 + g.n * p.T_N;
+    const bool whole = g.c0 == 0 && g.c1 == chunks;
+    if (whole) {
+      for (int j = 0; j < NT / 16; ++j) {
+        float v[16];
+        tmem_ld16(s.tmem_base + (uint32_t(32 * q) << 16) + uint32_t(buf * 64 + 16 * j), v);
+        umma_epi16(s, p, m0, rows_m, out_col0, row, q, lane, cw, j, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s.tmem_free[buf]);
+      ++tb_k;
+      continue;
+    }
+    // partial piece: TMEM -> piece slot, release the accumulator early
+    float* mine = piece_ptr(p, w_in_task, g.first ? 0 : 1);
     for (int j = 0; j < NT / 16; ++j) {
       float v[16];
       tmem_ld16(s.tmem_base + (uint32_t(32 * q) << 16) + uint32_t(buf * 64 + 16 * j), v);
-      if (p.epilogue == MK_EPI_LOGITS) {
-        float* y = reinterpret_cast<float*>(p.y);
-        const int col = out_col0 + row;
-        const bool valid_col = col < p.y_cols;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int bi = 16 * j + i;
-          float val = valid_col ? v[i] : -INFINITY;
-          if (y && valid_col && bi < rows_m) y[size_t(m0 + bi) * p.ldy + col] = val;
-          int idx = col;
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) {
-            const float v2 = __shfl_xor_sync(0xffffffffu, val, off);
-            const int i2 = __shfl_xor_sync(0xffffffffu, idx, off);
-            if (v2 > val || (v2 == val && i2 < idx)) { val = v2; idx = i2; }
-          }
-          if (lane == 0 && bi < rows_m) {
-            float& bv = s.amx_val[cw][m0 + bi];
-            int& bx = s.amx_idx[cw][m0 + bi];
-            if (val > bv || (val == bv && idx < bx)) { bv = val; bx = idx; }
-          }
-        }
-      } else if (silu) {
-        // rows 32q..32q+15 are gate rows 16q.., rows 32q+16.. the matching up rows
-        uint16_t* y = reinterpret_cast<uint16_t*>(p.y);
-        const int col = out_col0 + 16 * q + (lane & 15);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float u = __shfl_down_sync(0xffffffffu, v[i], 16);
-          const int bi = 16 * j + i;
-          if (lane < 16 && bi < rows_m)
-            y[size_t(m0 + bi) * p.ldy + col] = f2bf(v[i] / (1.f + __expf(-v[i])) * u);
-        }
-      } else {
-        uint16_t* y = reinterpret_cast<uint16_t*>(p.y);
-        const uint16_t* res = reinterpret_cast<const uint16_t*>(p.res);
-        const int col = out_col0 + row;
-        float rv[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int bi = 16 * j + i;
-          rv[i] = (p.epilogue == MK_EPI_RESIDUAL && bi < rows_m)
-                      ? bf2f(ldg16_cg(res + size_t(m0 + bi) * p.ldres + col)) : 0.f;
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int bi = 16 * j + i;
-          if (bi < rows_m) y[size_t(m0 + bi) * p.ldy + col] = f2bf(v[i] + rv[i]);
-        }
-      }
+      for (int i = 0; i < 16; ++i)
+        if (16 * j + i < rows_m) __stcg(mine + (16 * j + i) * 128 + row, v[i]);
     }
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&s.tmem_free[buf]);
     ++tb_k;
+    const PieceInfo pi = tile_pieces(p, a.W, g.tile);
+    __threadfence();
+    bar_sync(2, 128);
+    if (et == 0) {
+      const uint32_t old = atom_acq_rel_add(&a.sub_ctr[p.tile_ctr0 + g.tile], 1u);
+      s.epi_last = (old + 1 == uint32_t(pi.n) * a.epoch) ? 1 : 0;
+    }
+    bar_sync(2, 128);
+    const int last = s.epi_last;
+    bar_sync(2, 128);                     // epi_last reusable by the next segment
+    if (!last) continue;
+    __threadfence();
+    for (int j = 0; j < NT / 16; ++j) {
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = 0.f;
+      for (int w = pi.first_w; w <= pi.last_w; ++w) {
+        if (pi.empty(w)) continue;
+        const float* src = piece_ptr(p, w, w == pi.first_w ? pi.slot0 : 0);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (16 * j + i < rows_m) v[i] += __ldcg(src + (16 * j + i) * 128 + row);
+      }
+      umma_epi16(s, p, m0, rows_m, out_col0, row, q, lane, cw, j, v);
+    }
   }
 }
 
@@ -922,13 +1359,24 @@ __device__ void run_gemm_umma(const KArgs& a, Smem& s, Ring& r, const mk_task& t
       s.amx_idx[e / kAmaxRows][e % kAmaxRows] = 0x7fffffff;
     }
   }
-  // count the unit's ring slots and hand the job to the MMA warp
-  int n_tiles_here = 0;
+  // count the unit's segments and ring slots, hand the job to the MMA warp
+  int n_seg = 0;
+  long long n_slots = 0;
   {
-    TileIter it;
+    SegIter it;
     it.init(p, a.W, w_in_task);
-    int m, n;
-    while (it.next(m, n)) ++n_tiles_here;
+    Seg g;
+    while (it.next(g)) {
+      ++n_seg; n_slots += g.c1 - g.c0;
+      if (ct == 0 && a.tile_log) {
+        unsigned long long at = atomicAdd(a.tile_cursor, 1ull);
+        if ((long long)at < a.tile_cap) {
+          int32_t* rec = a.tile_log + at * 4;
+          rec[0] = tix; rec[1] = (t.level == MK_LEVEL_CHIPLET ? t.die * a.W : 0) + worker;
+          rec[2] = g.m; rec[3] = g.n;
+        }
+      }
+    }
   }
   bar_sync(1, kCons);
   if (ct == 0) {
@@ -936,10 +1384,10 @@ __device__ void run_gemm_umma(const KArgs& a, Smem& s, Ring& r, const mk_task& t
     mbar_arrive(&s.job_full);
   }
   if (ct < 128) umma_stage(a, s, p, w_in_task, ct, xs_k);
-  else umma_epilogue(a, s, p, w_in_task, ct - 128 + 128, tb_k);
+  else umma_epilogue(a, s, p, w_in_task, ct, tb_k);
   bar_sync(1, kCons);
-  r.k += uint32_t(n_tiles_here) * uint32_t(p.K / p.T_K);
-  if (ct == 0) tiles += n_tiles_here;
+  r.k += uint32_t(n_slots);
+  if (ct == 0) tiles += n_seg;
   if (p.epilogue == MK_EPI_LOGITS) {
     const int slot = p.amax_base + w_in_task;
     // a CU tile task owns only its m-tile's rows of the shared slot
@@ -960,6 +1408,7 @@ __device__ void run_gemm_umma(const KArgs& a, Smem& s, Ring& r, const mk_task& t
   }
 }
 
+template <int F>
 __device__ void run_gemm(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
                          const mk_task& t, int worker, int gw, int tix, int ct,
                          unsigned long long& tiles) {
@@ -979,7 +1428,15 @@ __device__ void run_gemm(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   else if (rows <= 4) gemm_task<4, XSV>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles); \
   else if (rows <= 8) gemm_task<8, XSV>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles); \
   else gemm_task<16, XSV>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles);
-  if (p.stage_x) { MK_GEMM_NB(true) } else { MK_GEMM_NB(false) }
+  if ((F & kFeatKsplit) && p.ksplit) {
+#define MK_GEMM_KS(XSV)                                                                 \
+  if (rows <= 1) gemm_task_ks<1, XSV>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles);     \
+  else if (rows <= 2) gemm_task_ks<2, XSV>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles); \
+  else if (rows <= 4) gemm_task_ks<4, XSV>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles); \
+  else gemm_task_ks<8, XSV>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles);
+    if (p.stage_x) { MK_GEMM_KS(true) } else { MK_GEMM_KS(false) }
+#undef MK_GEMM_KS
+  } else if (p.stage_x) { MK_GEMM_NB(true) } else { MK_GEMM_NB(false) }
 #undef MK_GEMM_NB
 }
 
@@ -1538,6 +1995,7 @@ __device__ void mailbox_warp(const KArgs& a, Smem& s, int g, int worker) {
   }
 }
 
+template <int F>
 __device__ void ring_warp(const KArgs& a, Smem& s, uint8_t* ring, int worker) {
   if ((threadIdx.x & 31) != 0) return;
   const uint64_t pol = policy_evict_first();
@@ -1547,7 +2005,7 @@ __device__ void ring_warp(const KArgs& a, Smem& s, uint8_t* ring, int worker) {
     if (!mbar_wait(a, &s.tq_full[qi], (q / kTQ) & 1, -8)) return;
     const int4 ent = s.tq[qi];
     if (ent.x < 0) return;
-    SlotIter it;
+    SlotIter<F> it;
     it.init(a, a.tasks[ent.x], ent.y, ent.z, worker);
     const void* src;
     uint32_t bytes;
@@ -1565,6 +2023,7 @@ __device__ void ring_warp(const KArgs& a, Smem& s, uint8_t* ring, int worker) {
   }
 }
 
+template <int F>
 __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int worker) {
   const int ct = threadIdx.x - kProdThreads;
   const int gw = g * a.W + worker;
@@ -1585,17 +2044,19 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
       if (ent.x >= 0) {
         const mk_task& t = a.tasks[ent.x];
         const int waits[2] = {t.wait0, t.wait1};
+        uint32_t polls = 0;
         for (int k = 0; k < 2; ++k) {
           const int e = waits[k];
           if (e < 0) continue;
           const uint32_t target = uint32_t(a.ev_req[e]) * a.epoch;
           Spin sp;
           for (;;) {
-            ++n_poll;
+            ++polls;
             if ((int32_t)(ld_acquire(&a.ev_ctr[e]) - target) >= 0) break;
             if (!sp.ok(a, e)) break;
           }
         }
+        n_poll += polls;
         if (a.log) t_start = globaltimer();
       }
       s.cur = ent;
@@ -1607,10 +2068,13 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
     const mk_task& t = a.tasks[ent.x];
     switch (t.op) {
       case MK_OP_GEMM:
-        if (P<mk_gemm_params>(a, t)->body == MK_BODY_UMMA)
-          run_gemm_umma(a, s, r, t, ent.x, worker, ct, xs_k, tb_k, n_tiles);
-        else
-          run_gemm(a, s, ring, r, t, worker, gw, ent.x, ct, n_tiles);
+        if constexpr ((F & kFeatUmma) != 0) {
+          if (P<mk_gemm_params>(a, t)->body == MK_BODY_UMMA) {
+            run_gemm_umma(a, s, r, t, ent.x, worker, ct, xs_k, tb_k, n_tiles);
+            break;
+          }
+        }
+        run_gemm<F>(a, s, ring, r, t, worker, gw, ent.x, ct, n_tiles);
         break;
       case MK_OP_RMSNORM: run_rmsnorm(a, s, t, ent.y, ent.z, ct); break;
       case MK_OP_ATTN_PARTIAL: run_attn_partial(a, s, ring, r, t, ent.y, ent.z, ct); break;
@@ -1664,7 +2128,8 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) megakernel(const KArgs a) {
+template <int F>
+__global__ void __launch_bounds__(kThreads, 1) megakernel(const __grid_constant__ KArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem& s = *reinterpret_cast<Smem*>(smem_raw);
   uint8_t* ring = smem_raw + kRingOffset;
@@ -1693,7 +2158,7 @@ __global__ void __launch_bounds__(kThreads, 1) megakernel(const KArgs a) {
   }
   const int worker = rank - 1;
   if (worker >= a.W) return;             // extra SMs of the larger die idle
-  if (a.use_umma) {                      // TMEM for the tcgen05 accumulators
+  if ((F & kFeatUmma) && a.use_umma) {   // TMEM for the tcgen05 accumulators
     if ((threadIdx.x >> 5) == 2) {
       tmem_alloc(&s.tmem_base, kTmemCols);
       tmem_relinquish();
@@ -1706,17 +2171,19 @@ __global__ void __launch_bounds__(kThreads, 1) megakernel(const KArgs a) {
   // drops to kProdRegs, the two consumer warpgroups grow to kConsRegs
   if (threadIdx.x < kProdThreads) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(kProdRegs));
-    if (threadIdx.x < 32) ring_warp(a, s, ring, worker);
+    if (threadIdx.x < 32) ring_warp<F>(a, s, ring, worker);
     else if (threadIdx.x < 64) mailbox_warp(a, s, g, worker);
     else if (threadIdx.x < 96 && a.use_umma) {
-      if ((threadIdx.x & 31) == 0) mma_warp(a, s, ring);
-      __syncwarp();
-      tc_fence_after();
-      tmem_dealloc(s.tmem_base, kTmemCols);
+      if constexpr ((F & kFeatUmma) != 0) {
+        if ((threadIdx.x & 31) == 0) mma_warp(a, s, ring);
+        __syncwarp();
+        tc_fence_after();
+        tmem_dealloc(s.tmem_base, kTmemCols);
+      }
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(kConsRegs));
-    consumers(a, s, ring, g, worker);
+    consumers<F>(a, s, ring, g, worker);
   }
 }
 
@@ -1787,6 +2254,8 @@ struct mk_handle {
   double watchdog_s = 5.0;
   int debug = 0;
   int use_umma = 0;
+  int feat = 0;                 // kFeat* bits of the graph -> kernel instance
+  const void* kernel = nullptr;
   // device buffers
   mk_task* d_tasks = nullptr;
   mk_unit* d_units = nullptr;
@@ -1813,6 +2282,12 @@ struct mk_handle {
   long long tile_cap = 0;
   std::vector<int32_t> group_size;
 };
+
+static const void* kernel_for(int feat) {
+  // two instances: the plain CUDA-core graph, and everything else
+  if ((feat & (kFeatUmma | kFeatKsplit)) == 0) return (const void*)megakernel<0>;
+  return (const void*)megakernel<kFeatUmma | kFeatKsplit>;
+}
 
 template <typename T>
 static int dalloc(T** p, size_t n) {
@@ -1981,6 +2456,18 @@ static int validate_graph(const mk_graph_desc* g) {
     if (t.op == MK_OP_GEMM) {
       const mk_gemm_params* p = reinterpret_cast<const mk_gemm_params*>(
           static_cast<const uint8_t*>(g->params) + t.param_off);
+      if (p->ksplit) {
+        const int R = p->T_N * (p->epilogue == MK_EPI_SILU ? 2 : 1);
+        const long long tiles = (long long)((p->M + p->T_M - 1) / p->T_M) * (p->N / std::max(R, 1));
+        const int need = p->body == MK_BODY_UMMA ? 128 * ((std::min(p->T_M, p->M) + 15) / 16 * 16)
+                                                 : R * p->T_M;
+        const int rows = std::min(p->T_M, p->M);
+        const bool fast = (rows <= 1 && R == 8 && p->T_K == 1024) || (rows <= 4 && R == 16 && p->T_K == 512) ||
+                          (rows <= 8 && R == 32 && p->T_K == 256);
+        if (t.level != MK_LEVEL_CHIPLET || !p->kpart || p->piece_floats < need || p->tile_ctr0 < 0 ||
+            p->tile_ctr0 + tiles > g->n_sub_ctrs || (p->body == MK_BODY_GEMV && !fast))
+          return fail(MK_ERR_CONFIG, "k-split gemm task " + std::to_string(i) + " has bad piece/counter setup");
+      }
       if (p->body == MK_BODY_UMMA) {
         const int R = p->T_N * (p->epilogue == MK_EPI_SILU ? 2 : 1);
         if (R != 128 || p->T_K != 64 || p->K % 64 || p->N % 128 || p->T_M > 64 || p->stage_x ||
@@ -2106,9 +2593,18 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
   CK(cudaMemset(h->d_stats, 0, 16 * sizeof(unsigned long long)));
   CK(cudaMemset(h->d_log_cursor, 0, sizeof(unsigned long long)));
   CK(cudaMemset(h->d_tile_cursor, 0, sizeof(unsigned long long)));
-  CK(cudaFuncSetAttribute(megakernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
+  for (int i = 0; i < g->n_tasks; ++i) {
+    const mk_task& t = g->tasks[i];
+    if (t.op != MK_OP_GEMM) continue;
+    const mk_gemm_params* gp =
+        reinterpret_cast<const mk_gemm_params*>(static_cast<const uint8_t*>(g->params) + t.param_off);
+    if (gp->body == MK_BODY_UMMA) h->feat |= kFeatUmma;
+    if (gp->ksplit) h->feat |= kFeatKsplit;
+  }
+  h->kernel = kernel_for(h->feat);
+  CK(cudaFuncSetAttribute(h->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
   int occ = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, megakernel, kThreads, kSmemBytes));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, h->kernel, kThreads, kSmemBytes));
   if (occ != 1) {
     delete h;
     return fail(MK_ERR_CONFIG, "megakernel occupancy is " + std::to_string(occ) + ", need exactly 1");
@@ -2146,7 +2642,7 @@ int mk_step(mk_handle* h, void* stream) {
   a.debug = h->debug;
   a.use_umma = h->use_umma;
   void* args[] = {&a};
-  CK(cudaLaunchCooperativeKernel((const void*)megakernel, dim3(h->num_sms), dim3(kThreads), args,
+  CK(cudaLaunchCooperativeKernel(h->kernel, dim3(h->num_sms), dim3(kThreads), args,
                                  kSmemBytes, static_cast<cudaStream_t>(stream)));
   return MK_OK;
 }

@@ -44,6 +44,27 @@ def is_umma_tile(tile, fused: bool) -> bool:
     return t_k == 64 and t_n * (2 if fused else 1) == 128
 
 
+KSPLIT_MIN_BALANCE = 0.85
+
+
+def gemv_fast_shape(batch_rows: int, rows: int, t_k: int) -> bool:
+    """The register-resident GEMV tile shapes (csrc gemm_tile_fast): the only
+    CUDA-core shapes with a K-split variant."""
+    return ((batch_rows <= 1 and rows == 8 and t_k == 1024)
+            or (batch_rows <= 4 and rows == 16 and t_k == 512)
+            or (batch_rows <= 8 and rows == 32 and t_k == 256))
+
+
+def ksplit_pays(tiles: int, workers: int) -> bool:
+    """K-split a die task only when whole-tile round-robin ownership
+    (schedule(), traversal.py:125-202) would leave the die's workers
+    unbalanced: tiles / (rounds * workers) below KSPLIT_MIN_BALANCE.  Whole
+    tiles keep the concurrent workers on adjacent weight tiles (one DRAM
+    sweep) and need no partial-sum exchange."""
+    rounds = _cdiv(tiles, workers)
+    return tiles / (rounds * workers) < KSPLIT_MIN_BALANCE
+
+
 @dataclass
 class LoweringOptions:
     sched_mode: int = L.SCHED_PER_DIE
@@ -58,8 +79,11 @@ class LoweringOptions:
                                    # activation staging when the rows fit
     bypass_noop: bool = True       # consumers of a fused (no-op) norm task wait
                                    # on that task's own predecessor event
+    ksplit: bool = True            # die tasks: K-split slot ranges per worker
+                                   # instead of whole tiles
 
 XS_BYTES = 32768                   # kXsBytes in mk_kernel.cu
+PIECE_FLOATS = 128 * 64            # K-split piece: 128 weight rows x 64 batch rows
 
 
 @dataclass
@@ -176,9 +200,21 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         return min(tile[0], M) * K * 2 <= XS_BYTES
 
     def gemm_params(w, x, y, res, M, K, N, tile, ldx, ldy, ldres, col0, epi,
-                    xcd, tm=-1, tn=-1, amax_base=0, gamma=None, y_cols=None):
+                    xcd, tm=-1, tn=-1, amax_base=0, gamma=None, y_cols=None,
+                    ksplit=False):
         p = L.GemmParams()
         umma = is_umma_tile(tile, epi == L.EPI_SILU)
+        rows = tile[1] * (2 if epi == L.EPI_SILU else 1)
+        if ksplit and not ksplit_pays(_cdiv(M, tile[0]) * (N // rows), opts.workers):
+            ksplit = False
+        if ksplit and not umma and not gemv_fast_shape(min(tile[0], M), rows, tile[2]):
+            ksplit = False
+        if ksplit:
+            p.ksplit = 1
+            p.tile_ctr0 = n_sub[0]
+            n_sub[0] += _cdiv(M, tile[0]) * (N // rows)
+            p.piece_floats = PIECE_FLOATS
+            p.kpart = _ptr(bufs.kpart, xcd * opts.workers * 2 * PIECE_FLOATS)
         p.body = L.BODY_UMMA if umma else L.BODY_GEMV
         p.stage_x = 0 if umma else (1 if stages(M, K, tile) else 0)
         p.y_cols = y_cols if y_cols is not None else (1 << 30)
@@ -236,6 +272,7 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         return None
 
     gu_fused = g.mode == "chiplet"
+    ksplit = opts.ksplit and per_die and bufs.kpart is not None
     fuse = opts.fuse_norm and all(
         stages(B, d, tl) and not is_umma_tile(tl, f)
         for tl, f in ((gemm_tile_of(OpKind.QKV_PROJ), False),
@@ -312,7 +349,7 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                 col0 = xd * (n_loc // 2 if epi == L.EPI_SILU else n_loc)
                 po = gemm_params(_ptr(w, xd * n_loc * K), _ptr(x), _ptr(y),
                                  _ptr(res), M, K, n_loc, tile, ldx, ldy, d,
-                                 col0, epi, xd, gamma=gamma)
+                                 col0, epi, xd, gamma=gamma, ksplit=ksplit)
                 add_task(t.id, gi, L.OP_GEMM, level, xd, wait, t.signal_event,
                          po, layer, n_items=0)
             else:
@@ -370,7 +407,7 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                              B, d, n_loc, (t_m, t_n, t_k), d, V, d,
                              xd * n_loc, L.EPI_LOGITS, xd,
                              amax_base=xd * opts.workers, gamma=lm_gamma,
-                             y_cols=spec.vocab)
+                             y_cols=spec.vocab, ksplit=ksplit)
             add_task(f"lm_head.x{xd}", -1, L.OP_GEMM, L.LEVEL_CHIPLET, xd,
                      lm_wait, "e.lm_head", po, n_layers, n_items=0)
         required[ev_index["e.lm_head"]] = X

@@ -28,8 +28,8 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _lib as L
-from .lowering import LoweringOptions, lower
-from .analytics import UMMA_MIN_BATCH
+from .lowering import PIECE_FLOATS, LoweringOptions, lower
+from .analytics import UMMA_MIN_BATCH, default_t_m
 from .machine import b200_from_probe
 from .taskgraph import OpKind, TaskGraph, TaskLevel
 from .traversal import Distribution, Traversal
@@ -109,6 +109,7 @@ class DeviceState:
     amax_val: torch.Tensor = None
     amax_idx: torch.Tensor = None
     partial: torch.Tensor = None
+    kpart: torch.Tensor = None
     tokens: torch.Tensor = None
     out_tokens: torch.Tensor = None
     positions: torch.Tensor = None
@@ -200,7 +201,8 @@ class Megakernel:
                  distribution: Distribution = Distribution.M_TILE,
                  sched: str = "per_die", topo: L.Topology | None = None,
                  fanout: bool = True, lm_tile=None, device: int = 0,
-                 keep_logits: bool = True, watchdog_s: float = 10.0):
+                 keep_logits: bool = True, watchdog_s: float = 10.0,
+                 ksplit: bool = True):
         if not torch.cuda.is_available():
             raise RuntimeError("Megakernel needs a CUDA device (no CPU fallback)")
         self.lib = L.load()
@@ -230,6 +232,11 @@ class Megakernel:
         self.state = build_state(g, weights, t_max, lm_tile, amax_slots,
                                  device=f"cuda:{device}",
                                  keep_logits=keep_logits)
+        if per_die and ksplit:
+            # K-split pieces: [die][worker][first/last segment][128 x 64] fp32
+            self.state.kpart = torch.zeros(n_dies * workers * 2 * PIECE_FLOATS,
+                                           device=f"cuda:{device}", dtype=torch.float32)
+        opts.ksplit = ksplit
         self.lowered = lower(g, self.spec, self.state, opts)
         run_topo = topo if per_die else flat_topology(topo.num_sms)
         self._desc = self.lowered.desc()
@@ -319,12 +326,15 @@ class Megakernel:
             pass
 
 
-def _default_lm_tile(spec: Qwen3Spec, batch: int, t_m: int = 16):
+def _default_lm_tile(spec: Qwen3Spec, batch: int, t_m: int | None = None):
     """LM-head tile: the tcgen05 body (128 x 64, vocab padded to 256) from
     UMMA_MIN_BATCH rows on, else the warp-row GEMV rule of gemv_tiles."""
+    if t_m is None:
+        t_m = default_t_m(batch)
     rows = min(batch, t_m)
     if rows >= UMMA_MIN_BATCH and spec.hidden % 64 == 0:
         return (t_m, 128, 64)
+    t_m = min(t_m, 16)
     t_n = 16 if rows <= 4 else 32
     while (spec.vocab // 2) % t_n and t_n > 8:
         t_n //= 2

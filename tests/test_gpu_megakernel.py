@@ -104,19 +104,20 @@ def test_toy_decode_matches_oracle(topo, machine, mode, sched, B):
     assert worst < RTOL
 
 
+@pytest.mark.parametrize("ksplit", [True, False])
 @pytest.mark.parametrize("dist,trav", [("m_tile", "m_major_windowed"),
                                        ("m_split", "m_major_windowed"),
                                        ("m_tile", "n_major")])
-def test_toy_batch_tiles_all_distributions(topo, machine, dist, trav):
+def test_toy_batch_tiles_all_distributions(topo, machine, dist, trav, ksplit):
     """B=20 > T_M=16: two m-tiles, every traversal/distribution computes the
-    same numbers."""
+    same numbers, with and without the K-split range partition."""
     from paper_2604_15379_b200 import Distribution, Traversal
     from paper_2604_15379_b200.runtime import Megakernel
     from paper_2604_15379_b200.weights import Qwen3Spec, Qwen3Weights
     w = Qwen3Weights.random(Qwen3Spec.toy(), seed=12)
     g = _toy_graph(machine, "chiplet", 20)
     mk = Megakernel(g, w, t_max=48, topo=topo, traversal=Traversal(trav),
-                    distribution=Distribution(dist))
+                    distribution=Distribution(dist), ksplit=ksplit)
     worst, _ = _decode_vs_oracle(mk, w, 20, steps=5, t_max=48)
     mk.close()
     assert worst < RTOL
@@ -213,7 +214,7 @@ def test_device_tile_loop_matches_reference_schedule(topo, machine):
     B = 40
     for dist in (Distribution.M_TILE, Distribution.M_SPLIT):
         g = _toy_graph(machine, "chiplet", B, layers=1)
-        mk = Megakernel(g, w, t_max=16, topo=topo, distribution=dist)
+        mk = Megakernel(g, w, t_max=16, topo=topo, distribution=dist, ksplit=False)
         mk.enable_tile_log(1 << 15)
         mk.step(list(range(B)))
         recs, n = mk.read_tile_log(1 << 15)
@@ -263,7 +264,7 @@ def test_watchdog_reports_deadlock(topo, machine):
     lib.mk_destroy(h)
 
 
-def _mini(machine, mode, B, layers=2):
+def _mini(machine, mode, B, layers=2, t_m=None):
     """Qwen3-shaped mini model whose widths divide the 128-row tcgen05 tiles."""
     from paper_2604_15379_b200 import build_decoder_layer
     from paper_2604_15379_b200.analytics import device_tiles
@@ -272,25 +273,115 @@ def _mini(machine, mode, B, layers=2):
     m = ModelConfig(hidden_dim=512, ffn_dim=1024, num_layers=layers, q_heads=4, kv_heads=2,
                     dtype_bytes=2)
     spec = Qwen3Spec(512, 1024, layers, 4, 2, 128, 1024)
-    g = build_decoder_layer(m, machine, mode, B, tile_overrides=device_tiles(m, machine, mode, B),
+    g = build_decoder_layer(m, machine, mode, B,
+                            tile_overrides=device_tiles(m, machine, mode, B, t_m=t_m),
                             layers=layers)
     return g, spec
 
 
-@pytest.mark.parametrize("mode,sched", [("chiplet", "per_die"), ("standard", "flat")])
-@pytest.mark.parametrize("B,dist", [(16, "m_tile"), (32, "m_tile"), (48, "m_split"), (64, "m_tile")])
-def test_tcgen05_decode_matches_oracle(topo, machine, mode, sched, B, dist):
-    """Batch >= 16: linear layers and the LM head run on tcgen05.mma with TMEM
-    accumulators (GemmParams.body == MK_BODY_UMMA)."""
-    import ctypes
+@pytest.mark.parametrize("B", [1, 4, 8])
+@pytest.mark.parametrize("ksplit", [True, False])
+def test_gemv_ksplit_decode_matches_oracle(topo, machine, B, ksplit):
+    """CUDA-core GEMV body (B <= 8) on the mini model: K-chunks per tile > 1,
+    so the K-split ranges cut tiles into pieces."""
+    from paper_2604_15379_b200.runtime import Megakernel
+    from paper_2604_15379_b200.weights import Qwen3Weights
+    g, spec = _mini(machine, "chiplet", B)
+    w = Qwen3Weights.random(spec, seed=32)
+    mk = Megakernel(g, w, t_max=40, topo=topo, ksplit=ksplit, watchdog_s=5.0)
+    worst, _ = _decode_vs_oracle(mk, w, B, steps=6, t_max=40)
+    mk.close()
+    assert worst < RTOL
+
+
+def _range_segments(mt, nt, chunks, W, w, trav, dist, xcd):
+    """Host restatement of the device K-split walk (RangeIter)."""
+    S = mt * nt * chunks
+    s, s1 = S * w // W, S * (w + 1) // W
+    out = []
+    while s < s1:
+        idx, c0 = divmod(s, chunks)
+        c1 = min(chunks, c0 + (s1 - s))
+        if dist == "m_split":
+            m, n = (xcd % mt + idx // nt) % mt, idx % nt
+        elif trav == "m_major_windowed":
+            m, n = idx % mt, idx // mt
+        else:
+            m, n = idx // nt, idx % nt
+        out.append((m, n, c0, c1))
+        s += c1 - c0
+    return out
+
+
+@pytest.mark.parametrize("dist", ["m_tile", "m_split"])
+def test_ksplit_segments_cover_every_slot_once(topo, machine, dist):
+    """Device K-split tile log == host restatement, and the segments of all
+    workers cover every (tile, K-chunk) slot of every die task exactly once."""
     from paper_2604_15379_b200 import Distribution
     from paper_2604_15379_b200 import _lib as L
     from paper_2604_15379_b200.runtime import Megakernel
     from paper_2604_15379_b200.weights import Qwen3Weights
-    g, spec = _mini(machine, mode, B)
+    import ctypes
+    B = 40
+    g, spec = _mini(machine, "chiplet", B, layers=1, t_m=16)
+    w = Qwen3Weights.random(spec, seed=33)
+    mk = Megakernel(g, w, t_max=16, topo=topo, distribution=Distribution(dist))
+    mk.enable_tile_log(1 << 16)
+    mk.step(list(range(B)))
+    recs, n = mk.read_tile_log(1 << 16)
+    low = mk.lowered
+    W = low.workers
+    checked = 0
+    for ti in range(len(low.tasks)):
+        t = low.tasks[ti]
+        if t.level != 2 or t.op != L.OP_GEMM:
+            continue
+        p = L.GemmParams.from_buffer_copy(
+            low.params[t.param_off:t.param_off + ctypes.sizeof(L.GemmParams)])
+        assert p.ksplit == 1
+        R = p.T_N * (2 if p.epilogue == L.EPI_SILU else 1)
+        mt, nt, chunks = -(-p.M // p.T_M), p.N // R, p.K // p.T_K
+        got = {}
+        for (tix, gw, m, nn) in recs:
+            if tix == ti:
+                got.setdefault(gw % W, []).append((m, nn))
+        cover = {}
+        for wk in range(W):
+            segs = _range_segments(mt, nt, chunks, W, wk, "m_major_windowed", dist, p.xcd)
+            assert got.get(wk, []) == [(m, nn) for m, nn, _, _ in segs], (ti, wk)
+            for m, nn, c0, c1 in segs:
+                for c in range(c0, c1):
+                    cover[(m, nn, c)] = cover.get((m, nn, c), 0) + 1
+        assert len(cover) == mt * nt * chunks and set(cover.values()) == {1}
+        checked += 1
+    assert checked >= 2 * 5
+    mk.close()
+
+
+@pytest.mark.parametrize("mode,sched", [("chiplet", "per_die"), ("standard", "flat")])
+@pytest.mark.parametrize("B,dist,t_m,ksplit", [(16, "m_tile", None, True),
+                                               (32, "m_tile", None, True),
+                                               (48, "m_split", None, True),
+                                               (64, "m_tile", None, True),
+                                               (64, "m_tile", None, False),
+                                               (64, "m_tile", 16, True),
+                                               (40, "m_split", 16, True)])
+def test_tcgen05_decode_matches_oracle(topo, machine, mode, sched, B, dist, t_m, ksplit):
+    """Batch >= 16: linear layers and the LM head run on tcgen05.mma with TMEM
+    accumulators (GemmParams.body == MK_BODY_UMMA); die tasks K-split across
+    the die's workers (partial pieces summed by the last piece)."""
+    import ctypes
+    from paper_2604_15379_b200 import Distribution
+    from paper_2604_15379_b200 import _lib as L
+    from paper_2604_15379_b200.runtime import Megakernel, _default_lm_tile
+    from paper_2604_15379_b200.weights import Qwen3Weights
+    if mode == "standard" and (t_m is not None or not ksplit):
+        pytest.skip("K-split / m-tile variants apply to die tasks")
+    g, spec = _mini(machine, mode, B, t_m=t_m)
     w = Qwen3Weights.random(spec, seed=31)
     mk = Megakernel(g, w, t_max=48, sched=sched, topo=topo,
-                    distribution=Distribution(dist), watchdog_s=5.0)
+                    distribution=Distribution(dist), watchdog_s=5.0, ksplit=ksplit,
+                    lm_tile=_default_lm_tile(spec, B, t_m))
     low = mk.lowered
     bodies = set()
     for i in range(len(low.tasks)):

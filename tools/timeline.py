@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--out", default="gpurun_out/timeline.json")
+    ap.add_argument("--t-m", type=int, default=None)
+    ap.add_argument("--no-ksplit", action="store_true")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     mk, model, spec, info = bench.build(args, 0)
