@@ -227,6 +227,13 @@ typedef struct mk_counters {
   uint64_t tiles;           /* GEMM tiles computed                            */
   uint64_t executions;      /* (unit, worker) executions                      */
   uint64_t steps;
+  /* diagnostics (mk_set_debug bit 2): SM cycles spent waiting, summed */
+  uint64_t wait_ring_empty; /* fetch warp: ring slot not yet released          */
+  uint64_t wait_mma_full;   /* MMA lane: weight slot not yet landed            */
+  uint64_t wait_mma_x;      /* MMA lane: activation chunk not yet landed       */
+  uint64_t wait_mma_tmem;   /* MMA lane: accumulator buffer not yet drained    */
+  uint64_t wait_epi_done;   /* epilogue: accumulator not yet complete          */
+  uint64_t mma_chunks;      /* K-chunks issued by MMA lanes                    */
 } mk_counters;
 
 /* Event-log record (one per executed unit per worker, plus scheduler
@@ -262,7 +269,8 @@ int64_t mk_log_read(mk_handle* h, mk_log_rec* out, int64_t max_records);
 int mk_tile_log_enable(mk_handle* h, int64_t capacity);
 int64_t mk_tile_log_read(mk_handle* h, int32_t* out4, int64_t max_records);
 int mk_set_watchdog(mk_handle* h, double seconds);
-/* Diagnostics only: bit0 = consumers skip GEMM math, bit1 = no TMA copies. */
+/* Diagnostics only: bit0 = consumers skip GEMM math, bit1 = no TMA copies,
+ * bit2 = count wait cycles (mk_counters wait_*). */
 int mk_set_debug(mk_handle* h, int flags);
 int mk_destroy(mk_handle* h);
 const char* mk_last_error(void);

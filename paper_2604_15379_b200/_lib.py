@@ -94,7 +94,9 @@ class GraphDesc(C.Structure):
 class Counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "dispatches", "mailbox_writes", "global_atomics", "local_atomics",
-        "fences", "fanout_atomics", "polls", "tiles", "executions", "steps")]
+        "fences", "fanout_atomics", "polls", "tiles", "executions", "steps",
+        "wait_ring_empty", "wait_mma_full", "wait_mma_x", "wait_mma_tmem",
+        "wait_epi_done", "mma_chunks")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

@@ -31,6 +31,8 @@
 //
 // Counters are monotone across launches: the event fires in step e (epoch,
 // 1-based) when counter >= required * e, so no per-step reset is needed.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <cooperative_groups.h>
 #include <cstdio>
@@ -52,13 +54,15 @@ constexpr int kProdThreads = 128;              // producer warpgroup (warp 0 fet
 constexpr int kThreads = kCons + kProdThreads;  // 12 warps = 3 warpgroups
 constexpr int kProdRegs = 88;                   // setmaxnreg budget: 128*88 + 256*200
 constexpr int kConsRegs = 200;                  //   = 62464 <= 65536
+constexpr int kProdRegsUmma = 152;              // tcgen05 instance: 128*152 + 256*176
+constexpr int kConsRegsUmma = 176;              //   = 64512 <= 65536
 constexpr int kSlotBytes = 16384;
 constexpr int kSlots = 10;
-constexpr int kXsBytes = 32768;                 // staged activations per task
+constexpr int kXsBytes = 49152;                 // staged activations per task / x ring
 constexpr int kMaxSplits = 128;                 // split-KV splits per row
 constexpr int kMaxPieces = 512;                 // splits x token subsets
-constexpr int kXStages = 4;                     // UMMA activation ring (8 KiB each)
-constexpr int kXStageBytes = 8192;              // 64 rows x 64 bf16, 128B-swizzled
+constexpr int kXStagesMax = 16;                 // UMMA activation ring: up to 16 stages of
+                                                //   NT rows x 64 bf16 (128B-swizzled), TMA-fed
 constexpr int kTmemCols = 128;                  // 2 accumulator buffers x 64 columns
 constexpr int kTQ = 32;                         // smem unit queue depth
 constexpr int kMailbox = 64;                    // mailbox depth per worker
@@ -73,7 +77,9 @@ constexpr int kAmaxRows = 64;
 
 enum StatIdx {
   S_DISPATCH = 0, S_MAILBOX, S_GLOBAL, S_LOCAL, S_FENCE, S_FANOUT, S_POLL,
-  S_TILES, S_EXEC, S_STEPS, S_N
+  S_TILES, S_EXEC, S_STEPS,
+  // debug bit 2: cycles spent waiting, per role (diagnostics)
+  S_W_RING_EMPTY, S_W_MMA_FULL, S_W_MMA_X, S_W_MMA_TMEM, S_W_EPI_DONE, S_MMA_CHUNKS, S_N
 };
 
 struct KArgs {
@@ -108,6 +114,9 @@ struct KArgs {
   uint32_t epoch;
   int debug;               // bit0: consumers skip GEMM math, bit1: fetch issues no TMA
   int use_umma;            // graph has tcgen05 GEMM tasks: allocate TMEM, run the MMA warp
+  const CUtensorMap* tmaps; // [n_tasks]: activation (x) tensor map of each tcgen05 GEMM task
+  int x_stages;            // x ring stages (kXsBytes / x_stage_bytes, <= kXStagesMax)
+  int x_stage_bytes;       // 128 * max NT over the graph's tcgen05 tasks
 };
 
 struct AttnScratch {
@@ -131,7 +140,7 @@ struct Smem {
   int piece_last;                   // K-split: this CTA summed the tile's pieces (GEMV)
   int epi_last;                     // K-split: same, tcgen05 epilogue warps
   // tcgen05 path
-  uint64_t xfull[kXStages], xempty[kXStages];
+  uint64_t xfull[kXStagesMax], xempty[kXStagesMax];
   uint64_t tile_done[2], tmem_free[2];
   uint64_t job_full;
   int4 job;                         // {task, worker-in-task, first ring slot, 0}
@@ -180,6 +189,44 @@ __device__ __forceinline__ bool mbar_wait(const KArgs& a, uint64_t* bar, uint32_
     if (!sp.ok(a, info)) return false;
   }
   return true;
+}
+
+// Latency-critical single-role waits (fetch warp, MMA warp): spin on the
+// non-suspending test_wait -- a suspended try_wait is only woken after a
+// delay, which paces a ring handshake at the wake-up latency.
+__device__ __forceinline__ bool mbar_spin(const KArgs& a, uint64_t* bar, uint32_t parity, int info) {
+  Spin sp;
+  while (!mbar_test_wait(bar, parity)) {
+    if (!sp.ok(a, info)) return false;
+  }
+  return true;
+}
+
+// Long waits of whole warps: lane 0 polls with a nanosleep backoff, the warp
+// then reconverges -- 32 spinning lanes per warp would flood the SM's
+// mbarrier unit and slow the latency-critical single-lane roles.
+__device__ __forceinline__ void mbar_wait_warp(const KArgs& a, uint64_t* bar, uint32_t parity, int info) {
+  if ((threadIdx.x & 31) == 0) {
+    Spin sp;
+    uint32_t ns = 32;
+    while (!mbar_try_wait(bar, parity)) {
+      if (!sp.ok(a, info)) break;
+      __nanosleep(ns);
+      ns = ns < 512 ? ns * 2 : 512;
+    }
+  }
+  __syncwarp();
+  mbar_try_wait(bar, parity);   // every lane observes the completed phase
+}
+
+// mbar_wait that adds the cycles it spent to `acc` when debug bit 2 is set
+__device__ __forceinline__ bool mbar_wait_p(const KArgs& a, uint64_t* bar, uint32_t parity, int info,
+                                            unsigned long long& acc) {
+  if (!(a.debug & 4)) return mbar_spin(a, bar, parity, info);
+  const long long t0 = clock64();
+  const bool ok = mbar_spin(a, bar, parity, info);
+  acc += (unsigned long long)(clock64() - t0);
+  return ok;
 }
 
 template <typename T>
@@ -1138,79 +1185,126 @@ __device__ __forceinline__ int umma_nt(const mk_gemm_params& p) {
   return (rows + 15) / 16 * 16;
 }
 
-__device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
-  uint32_t jq = 0, xs_k = 0, tb_k = 0;
-  const uint32_t ring_s = smem_u32(ring);
-  const uint32_t xring_s = smem_u32(s.u.xs);
+// The tcgen05 path runs on two producer warps with warp-uniform control flow
+// (a single diverged lane would leave the other 31 parked at a convergence
+// barrier); lane 0 of each issues.  The per-chunk paths are kept short --
+// they pace the whole die task: ring / x-stage indices and phases advance
+// incrementally (x_stages is a power of two), smem descriptors are offsets
+// of per-ring base descriptors.
+//
+// x-load warp (warp 3): for each job, TMA-loads the activation chunk of every
+// K-chunk the MMAs will consume into the x ring (x_stages deep), gated only
+// by the stage being released by the MMA that read it.
+__device__ void xload_warp(const KArgs& a, Smem& s) {
+  const bool leader = (threadIdx.x & 31) == 0;
+  const int XS = a.x_stages;                 // power of two
+  const int xs_shift = __ffs(XS) - 1;
+  const uint32_t XB = uint32_t(a.x_stage_bytes);
+  uint32_t xs_load = 0, jq = 0;
   for (;;) {
-    if (!mbar_wait(a, &s.job_full, jq & 1, -9)) return;
+    if (!mbar_wait(a, &s.job_full, jq & 1, -15)) break;
     ++jq;
     const int4 job = s.job;
-    if (job.x < 0) return;
-    const mk_task& t = a.tasks[job.x];
-    const mk_gemm_params& p = *P<mk_gemm_params>(a, t);
-    const int NT = umma_nt(p);
-    const uint32_t idesc = umma_idesc_bf16(128, NT);
-    uint32_t slot = uint32_t(job.z);
+    if (job.x < 0) break;
+    const mk_gemm_params& p = *P<mk_gemm_params>(a, a.tasks[job.x]);
+    const void* tmap = a.tmaps + job.x;
+    const uint32_t x_bytes = uint32_t(umma_nt(p)) * 128u;
+    // the consumers acquired the job's input event: order those generic
+    // writes before the async-proxy (TMA) reads of x
+    if (leader) fence_proxy_async_global();
+    SegIter lt;
+    lt.init(p, a.W, job.y);
+    Seg g;
+    while (lt.next(g)) {
+      const int row = g.m * p.T_M;
+      for (int c = g.c0; c < g.c1; ++c) {
+        const int xl = int(xs_load & uint32_t(XS - 1));
+        if (!mbar_spin(a, &s.xempty[xl], ((xs_load >> xs_shift) & 1) ^ 1, -13)) return;
+        if (leader) {
+          if (a.debug & 16) {          // diagnostics: no activation TMA
+            mbar_arrive(&s.xfull[xl]);
+          } else {
+            mbar_arrive_expect_tx(&s.xfull[xl], x_bytes);
+            tma_load_2d(reinterpret_cast<uint8_t*>(s.u.xs) + size_t(xl) * XB, tmap, c * 64, row,
+                        &s.xfull[xl]);
+          }
+        }
+        __syncwarp();
+        ++xs_load;
+      }
+    }
+  }
+}
+
+// MMA warp (warp 2): per K-chunk wait for the weight slot and the activation
+// stage, issue the four UMMA_K=16 MMAs into the segment's TMEM accumulator,
+// release both through tcgen05.commit; one commit per segment to tile_done.
+__device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
+  const bool leader = (threadIdx.x & 31) == 0;
+  const int XS = a.x_stages;                 // power of two
+  const int xs_shift = __ffs(XS) - 1;
+  const uint32_t XB = uint32_t(a.x_stage_bytes);
+  int ri = 0; uint32_t rph = 0;              // ring slot index / phase
+  uint32_t xs_mma = 0, tb_k = 0, jq = 0;
+  unsigned long long w_full = 0, w_x = 0, w_tmem = 0, n_chunks = 0;
+  const uint64_t adesc0 = umma_desc_sw128(smem_u32(ring));
+  const uint64_t bdesc0 = umma_desc_sw128(smem_u32(s.u.xs));
+  for (;;) {
+    if (!mbar_wait(a, &s.job_full, jq & 1, -9)) break;
+    ++jq;
+    const int4 job = s.job;
+    if (job.x < 0) break;
+    const mk_gemm_params& p = *P<mk_gemm_params>(a, a.tasks[job.x]);
+    const uint32_t idesc = umma_idesc_bf16(128, umma_nt(p));
+    // the job starts at the consumers' ring cursor (job.z)
+    ri = int(uint32_t(job.z) % kSlots);
+    rph = (uint32_t(job.z) / kSlots) & 1;
     SegIter it;
     it.init(p, a.W, job.y);
     Seg sg;
     while (it.next(sg)) {
       const int buf = tb_k & 1;
-      if (!mbar_wait(a, &s.tmem_free[buf], ((tb_k >> 1) & 1) ^ 1, -10)) return;
+      if (!mbar_wait_p(a, &s.tmem_free[buf], ((tb_k >> 1) & 1) ^ 1, -10, w_tmem)) return;
       tc_fence_after();
       const uint32_t d = s.tmem_base + uint32_t(buf * 64);
       for (int c = sg.c0; c < sg.c1; ++c) {
-        const int i = slot % kSlots;
-        const int xi = xs_k % kXStages;
-        if (!mbar_wait(a, &s.full[i], (slot / kSlots) & 1, -11)) return;
-        if (!mbar_wait(a, &s.xfull[xi], (xs_k / kXStages) & 1, -12)) return;
+        ++n_chunks;
+        const int xi = int(xs_mma & uint32_t(XS - 1));
+        if (!mbar_wait_p(a, &s.full[ri], rph, -11, w_full)) return;
+        if (!mbar_wait_p(a, &s.xfull[xi], (xs_mma >> xs_shift) & 1, -12, w_x)) return;
         tc_fence_after();
-        const uint32_t a_base = ring_s + uint32_t(i) * kSlotBytes;
-        const uint32_t b_base = xring_s + uint32_t(xi) * kXStageBytes;
+        if (leader) {
+          if (a.debug & 8) {             // diagnostics: no MMA, release at once
+            mbar_arrive_cnt(&s.empty[ri], kConsWarps);
+            mbar_arrive(&s.xempty[xi]);
+          } else {
+            const uint64_t ad = adesc0 + uint64_t(ri * (kSlotBytes >> 4));
+            const uint64_t bd = bdesc0 + uint64_t(xi * (XB >> 4));
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)   // UMMA_K = 16 bf16 = 32 bytes along the swizzled row
-          umma_bf16(d, umma_desc_sw128(a_base + kk * 32), umma_desc_sw128(b_base + kk * 32),
-                    idesc, (c != sg.c0 || kk != 0));
-#pragma unroll
-        for (int w = 0; w < kConsWarps; ++w) umma_commit(&s.empty[i]);   // ring slot: 8 arrivals
-        umma_commit(&s.xempty[xi]);
-        ++slot; ++xs_k;
+            for (int kk = 0; kk < 4; ++kk)   // UMMA_K = 16 bf16 = 32 B along the swizzled row
+              umma_bf16(d, ad + uint64_t(2 * kk), bd + uint64_t(2 * kk), idesc, (c != sg.c0 || kk != 0));
+            // ring slot: 8 arrivals (one per GEMV consumer warp); 7 now, the
+            // eighth from the commit when the MMAs have read the slot
+            mbar_arrive_cnt(&s.empty[ri], kConsWarps - 1);
+            umma_commit(&s.empty[ri]);
+            umma_commit(&s.xempty[xi]);
+          }
+        }
+        __syncwarp();
+        if (++ri == kSlots) { ri = 0; rph ^= 1; }
+        ++xs_mma;
       }
-      umma_commit(&s.tile_done[buf]);
+      if (leader) {
+        if (a.debug & 8) mbar_arrive(&s.tile_done[buf]);
+        else umma_commit(&s.tile_done[buf]);
+      }
+      __syncwarp();
       ++tb_k;
     }
   }
-}
-
-// Consumer warps 0-3: stage the activation chunks of every segment into the
-// x ring, 128B-swizzled K-major [NT rows][64], zero rows past the batch.
-__device__ void umma_stage(const KArgs& a, Smem& s, const mk_gemm_params& p, int w_in_task,
-                           int ct, uint32_t& xs_k) {
-  const int NT = umma_nt(p);
-  const uint16_t* x = reinterpret_cast<const uint16_t*>(p.x);
-  const int lane = ct & 31;
-  SegIter it;
-  it.init(p, a.W, w_in_task);
-  Seg g;
-  while (it.next(g)) {
-    const int m0 = g.m * p.T_M;
-    const int rows_m = min(p.T_M, p.M - m0);
-    for (int c = g.c0; c < g.c1; ++c) {
-      const int xi = xs_k % kXStages;
-      mbar_wait(a, &s.xempty[xi], ((xs_k / kXStages) & 1) ^ 1, -13);
-      uint8_t* xb = reinterpret_cast<uint8_t*>(s.u.xs) + size_t(xi) * kXStageBytes;
-      for (int sg = ct; sg < NT * 8; sg += 128) {
-        const int row = sg >> 3, ch = sg & 7;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (row < rows_m) v = ldg128_cg(x + size_t(m0 + row) * p.ldx + c * 64 + ch * 8);
-        *reinterpret_cast<uint4*>(xb + row * 128 + ((ch ^ (row & 7)) << 4)) = v;
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s.xfull[xi]);
-      ++xs_k;
-    }
+  if (leader && (a.debug & 4)) {
+    atomicAdd(&a.stats[S_W_MMA_FULL], w_full); atomicAdd(&a.stats[S_W_MMA_X], w_x);
+    atomicAdd(&a.stats[S_W_MMA_TMEM], w_tmem); atomicAdd(&a.stats[S_MMA_CHUNKS], n_chunks);
   }
 }
 
@@ -1271,8 +1365,9 @@ __device__ __forceinline__ void umma_epi16(Smem& s, const mk_gemm_params& p, int
   }
 }
 
-// Consumer warps 4-7 (CTA warps 8-11, TMEM lane quadrant q = warp % 4):
-// accumulator -> registers -> epilogue.  A K-split piece goes to the
+// All 8 consumer warps (CTA warps 4-11; TMEM lane quadrant q = warp % 4,
+// warps q and q+4 take alternate 16-column groups): accumulator ->
+// registers -> epilogue.  A K-split piece goes to the
 // worker's piece slot ([col][128 rows] fp32, coalesced); the last piece of a
 // tile sums all pieces in piece order and runs the epilogue.
 __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, int w_in_task,
@@ -1281,7 +1376,7 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
   const int lane = ct & 31;
   const int q = (ct >> 5) & 3;
   const int cw = ct >> 5;                 // consumer warp index (amx slot)
-  const int et = ct - 128;                // epilogue-group thread 0..127
+  const int half = ct >> 7;               // which column groups (j parity)
   const int chunks = p.K / p.T_K;
   SegIter it;
   it.init(p, a.W, w_in_task);
@@ -1290,13 +1385,17 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
     const int m0 = g.m * p.T_M;
     const int rows_m = min(p.T_M, p.M - m0);
     const int buf = tb_k & 1;
-    mbar_wait(a, &s.tile_done[buf], (tb_k >> 1) & 1, -14);
+    {
+      const long long t0 = (a.debug & 4) ? clock64() : 0;
+      mbar_wait_warp(a, &s.tile_done[buf], (tb_k >> 1) & 1, -14);
+      if ((a.debug & 4) && ct == 128) atomicAdd(&a.stats[S_W_EPI_DONE], (unsigned long long)(clock64() - t0));
+    }
     tc_fence_after();
     const int row = 32 * q + lane;        // weight row inside the tile
     const int out_col0 = p.y_col0 + g.n * p.T_N;
     const bool whole = g.c0 == 0 && g.c1 == chunks;
     if (whole) {
-      for (int j = 0; j < NT / 16; ++j) {
+      for (int j = half; j < NT / 16; j += 2) {
         float v[16];
         tmem_ld16(s.tmem_base + (uint32_t(32 * q) << 16) + uint32_t(buf * 64 + 16 * j), v);
         umma_epi16(s, p, m0, rows_m, out_col0, row, q, lane, cw, j, v);
@@ -1309,7 +1408,7 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
     }
     // partial piece: TMEM -> piece slot, release the accumulator early
     float* mine = piece_ptr(p, w_in_task, g.first ? 0 : 1);
-    for (int j = 0; j < NT / 16; ++j) {
+    for (int j = half; j < NT / 16; j += 2) {
       float v[16];
       tmem_ld16(s.tmem_base + (uint32_t(32 * q) << 16) + uint32_t(buf * 64 + 16 * j), v);
 #pragma unroll
@@ -1322,17 +1421,17 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
     ++tb_k;
     const PieceInfo pi = tile_pieces(p, a.W, g.tile);
     __threadfence();
-    bar_sync(2, 128);
-    if (et == 0) {
+    bar_sync(2, kCons);
+    if (ct == 0) {
       const uint32_t old = atom_acq_rel_add(&a.sub_ctr[p.tile_ctr0 + g.tile], 1u);
       s.epi_last = (old + 1 == uint32_t(pi.n) * a.epoch) ? 1 : 0;
     }
-    bar_sync(2, 128);
+    bar_sync(2, kCons);
     const int last = s.epi_last;
-    bar_sync(2, 128);                     // epi_last reusable by the next segment
+    bar_sync(2, kCons);                   // epi_last reusable by the next segment
     if (!last) continue;
     __threadfence();
-    for (int j = 0; j < NT / 16; ++j) {
+    for (int j = half; j < NT / 16; j += 2) {
       float v[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = 0.f;
@@ -1383,8 +1482,8 @@ __device__ void run_gemm_umma(const KArgs& a, Smem& s, Ring& r, const mk_task& t
     s.job = make_int4(tix, w_in_task, int(r.k), 0);
     mbar_arrive(&s.job_full);
   }
-  if (ct < 128) umma_stage(a, s, p, w_in_task, ct, xs_k);
-  else umma_epilogue(a, s, p, w_in_task, ct, tb_k);
+  umma_epilogue(a, s, p, w_in_task, ct, tb_k);
+  (void)xs_k;
   bar_sync(1, kCons);
   r.k += uint32_t(n_slots);
   if (ct == 0) tiles += n_seg;
@@ -1973,11 +2072,15 @@ __device__ void mailbox_warp(const KArgs& a, Smem& s, int g, int worker) {
     if (room) {
       Spin sp;
       const uint64_t* slotp = &a.mailbox[size_t(gw) * kMailbox + head % kMailbox];
+      // relaxed polling (ld.acquire would invalidate this SM's L1 on every
+      // iteration, evicting the other roles' stack data) + one fence
       for (;;) {
-        e = ld_acquire64(slotp);
+        e = ld_relaxed64(slotp);
         if ((e >> 24) == head + 1) break;
         if (!sp.ok(a, -5)) { e = kEnd; break; }
+        __nanosleep(64);
       }
+      fence_acq_rel_gpu();
       if ((e >> 24) == head + 1) {
         ++head;
         st_release64(&a.mb_head[gw], head);
@@ -1999,7 +2102,13 @@ template <int F>
 __device__ void ring_warp(const KArgs& a, Smem& s, uint8_t* ring, int worker) {
   if ((threadIdx.x & 31) != 0) return;
   const uint64_t pol = policy_evict_first();
-  uint32_t slot = 0;
+  int si = 0;                       // ring slot index / phase
+  uint32_t sph = 0;
+  unsigned long long w_empty = 0;
+  struct Flush {
+    const KArgs& a; unsigned long long& e;
+    __device__ ~Flush() { if (a.debug & 4) atomicAdd(&a.stats[S_W_RING_EMPTY], e); }
+  } flush{a, w_empty};
   for (uint32_t q = 0;; ++q) {
     const int qi = q % kTQ;
     if (!mbar_wait(a, &s.tq_full[qi], (q / kTQ) & 1, -8)) return;
@@ -2010,15 +2119,14 @@ __device__ void ring_warp(const KArgs& a, Smem& s, uint8_t* ring, int worker) {
     const void* src;
     uint32_t bytes;
     while (it.next(a, src, bytes)) {
-      const int i = slot % kSlots;
-      if (!mbar_wait(a, &s.empty[i], ((slot / kSlots) & 1) ^ 1, -2)) return;
+      if (!mbar_wait_p(a, &s.empty[si], sph ^ 1, -2, w_empty)) return;
       if (a.debug & 2) {
-        mbar_arrive(&s.full[i]);
+        mbar_arrive(&s.full[si]);
       } else {
-        mbar_arrive_expect_tx(&s.full[i], bytes);
-        bulk_g2s(ring + size_t(i) * kSlotBytes, src, bytes, &s.full[i], pol);
+        mbar_arrive_expect_tx(&s.full[si], bytes);
+        bulk_g2s(ring + size_t(si) * kSlotBytes, src, bytes, &s.full[si], pol);
       }
-      ++slot;
+      if (++si == kSlots) { si = 0; sph ^= 1; }
     }
   }
 }
@@ -2143,8 +2251,8 @@ __global__ void __launch_bounds__(kThreads, 1) megakernel(const __grid_constant_
     role[1] = rank;
     for (int i = 0; i < kSlots; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], kConsWarps); }
     for (int i = 0; i < kTQ; ++i) { mbar_init(&s.tq_full[i], 1); mbar_init(&s.tq_empty[i], 1); }
-    for (int i = 0; i < kXStages; ++i) { mbar_init(&s.xfull[i], 4); mbar_init(&s.xempty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&s.tile_done[i], 1); mbar_init(&s.tmem_free[i], 4); }
+    for (int i = 0; i < kXStagesMax; ++i) { mbar_init(&s.xfull[i], 1); mbar_init(&s.xempty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&s.tile_done[i], 1); mbar_init(&s.tmem_free[i], kConsWarps); }
     mbar_init(&s.job_full, 1);
     fence_mbar_init();
     if (blockIdx.x == 0) atomicAdd(&a.stats[S_STEPS], 1ull);
@@ -2170,19 +2278,25 @@ __global__ void __launch_bounds__(kThreads, 1) megakernel(const __grid_constant_
   // warp specialisation with register reallocation: the producer warpgroup
   // drops to kProdRegs, the two consumer warpgroups grow to kConsRegs
   if (threadIdx.x < kProdThreads) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(kProdRegs));
+    // the tcgen05 instance gives the producer roles (fetch warp, MMA lane:
+    // iterator state) more registers than the CUDA-core instance
+    if constexpr ((F & kFeatUmma) != 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(kProdRegsUmma));
+    else asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(kProdRegs));
     if (threadIdx.x < 32) ring_warp<F>(a, s, ring, worker);
     else if (threadIdx.x < 64) mailbox_warp(a, s, g, worker);
     else if (threadIdx.x < 96 && a.use_umma) {
       if constexpr ((F & kFeatUmma) != 0) {
-        if ((threadIdx.x & 31) == 0) mma_warp(a, s, ring);
+        mma_warp(a, s, ring);
         __syncwarp();
         tc_fence_after();
         tmem_dealloc(s.tmem_base, kTmemCols);
       }
+    } else if (a.use_umma) {
+      if constexpr ((F & kFeatUmma) != 0) xload_warp(a, s);
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(kConsRegs));
+    if constexpr ((F & kFeatUmma) != 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(kConsRegsUmma));
+    else asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(kConsRegs));
     consumers<F>(a, s, ring, g, worker);
   }
 }
@@ -2256,6 +2370,8 @@ struct mk_handle {
   int use_umma = 0;
   int feat = 0;                 // kFeat* bits of the graph -> kernel instance
   const void* kernel = nullptr;
+  CUtensorMap* d_tmaps = nullptr; // x tensor map per task (tcgen05 GEMMs)
+  int x_stages = 1, x_stage_bytes = 2048;
   // device buffers
   mk_task* d_tasks = nullptr;
   mk_unit* d_units = nullptr;
@@ -2504,6 +2620,52 @@ static int validate_graph(const mk_graph_desc* g) {
   return MK_OK;
 }
 
+// Activation tensor maps of the tcgen05 GEMM tasks: x is bf16 [M][ldx]; one
+// box = 64 K-elements x NT rows, 128B-swizzled (the UMMA K-major SW128
+// operand layout), rows past M zero-filled.
+static int build_tmaps(mk_handle* h, const mk_graph_desc* g) {
+  std::vector<CUtensorMap> maps(std::max(1, g->n_tasks));
+  memset(maps.data(), 0, maps.size() * sizeof(CUtensorMap));
+  int max_nt = 16;
+  bool any = false;
+  PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  for (int i = 0; i < g->n_tasks; ++i) {
+    const mk_task& t = g->tasks[i];
+    if (t.op != MK_OP_GEMM) continue;
+    const mk_gemm_params* p =
+        reinterpret_cast<const mk_gemm_params*>(static_cast<const uint8_t*>(g->params) + t.param_off);
+    if (p->body != MK_BODY_UMMA) continue;
+    if (!encode) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+      if (!fn || q != cudaDriverEntryPointSuccess) return fail(MK_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const int nt = (std::min(p->T_M, p->M) + 15) / 16 * 16;
+    max_nt = std::max(max_nt, nt);
+    cuuint64_t dims[2] = {cuuint64_t(p->K), cuuint64_t(p->M)};
+    cuuint64_t strides[1] = {cuuint64_t(p->ldx) * 2};
+    cuuint32_t box[2] = {64, cuuint32_t(nt)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(&maps[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(p->x), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(MK_ERR_CONFIG, "task " + std::to_string(i) + ": x tensor map rejected (" + std::to_string(int(r)) + ")");
+    any = true;
+  }
+  h->x_stage_bytes = max_nt * 128;
+  int xs = 1;                                       // power of two stages
+  while (xs * 2 <= kXStagesMax && (xs * 2) * h->x_stage_bytes <= kXsBytes) xs *= 2;
+  h->x_stages = xs;
+  if (any) {
+    CK(cudaMalloc(&h->d_tmaps, maps.size() * sizeof(CUtensorMap)));
+    CK(cudaMemcpy(h->d_tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+  }
+  return MK_OK;
+}
+
 static int reset_state(mk_handle* h) {
   CK(cudaMemset(h->d_ev_ctr, 0, sizeof(uint32_t) * std::max(1, h->n_events)));
   CK(cudaMemset(h->d_die_ctr, 0, sizeof(uint32_t) * std::max(1, h->n_events * h->n_sched)));
@@ -2574,7 +2736,7 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
   DA(h->d_die_of_sm, MK_MAX_SMS);
   DA(h->d_role_ctr, MK_MAX_DIES);
   DA(h->d_group_size, MK_MAX_DIES);
-  DA(h->d_stats, 16);
+  DA(h->d_stats, 32);
   DA(h->d_err, 2);
   DA(h->d_log_cursor, 1);
   DA(h->d_tile_cursor, 1);
@@ -2590,7 +2752,7 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
   CK(cudaMemcpy(h->d_die_of_sm, die_of_sm.data(), MK_MAX_SMS, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(h->d_group_size, h->group_size.data(), sizeof(int32_t) * MK_MAX_DIES,
                 cudaMemcpyHostToDevice));
-  CK(cudaMemset(h->d_stats, 0, 16 * sizeof(unsigned long long)));
+  CK(cudaMemset(h->d_stats, 0, 32 * sizeof(unsigned long long)));
   CK(cudaMemset(h->d_log_cursor, 0, sizeof(unsigned long long)));
   CK(cudaMemset(h->d_tile_cursor, 0, sizeof(unsigned long long)));
   for (int i = 0; i < g->n_tasks; ++i) {
@@ -2616,6 +2778,8 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
             MK_BODY_UMMA)
       h->use_umma = 1;
   }
+  rc = build_tmaps(h, g);
+  if (rc) { delete h; return rc; }
   rc = reset_state(h);
   if (rc) { delete h; return rc; }
   *out = h;
@@ -2641,6 +2805,9 @@ int mk_step(mk_handle* h, void* stream) {
   a.epoch = h->epoch;
   a.debug = h->debug;
   a.use_umma = h->use_umma;
+  a.tmaps = h->d_tmaps;
+  a.x_stages = h->x_stages;
+  a.x_stage_bytes = h->x_stage_bytes;
   void* args[] = {&a};
   CK(cudaLaunchCooperativeKernel(h->kernel, dim3(h->num_sms), dim3(kThreads), args,
                                  kSmemBytes, static_cast<cudaStream_t>(stream)));
@@ -2663,19 +2830,22 @@ int mk_sync(mk_handle* h) {
 int mk_counters_get(mk_handle* h, mk_counters* out) {
   if (!h || !out) return fail(MK_ERR_CONFIG, "null argument");
   CK(cudaSetDevice(h->device));
-  unsigned long long s[16];
+  unsigned long long s[32];
   CK(cudaMemcpy(s, h->d_stats, sizeof(s), cudaMemcpyDeviceToHost));
   out->dispatches = s[S_DISPATCH]; out->mailbox_writes = s[S_MAILBOX];
   out->global_atomics = s[S_GLOBAL]; out->local_atomics = s[S_LOCAL]; out->fences = s[S_FENCE];
   out->fanout_atomics = s[S_FANOUT]; out->polls = s[S_POLL]; out->tiles = s[S_TILES];
   out->executions = s[S_EXEC]; out->steps = s[S_STEPS];
+  out->wait_ring_empty = s[S_W_RING_EMPTY]; out->wait_mma_full = s[S_W_MMA_FULL];
+  out->wait_mma_x = s[S_W_MMA_X]; out->wait_mma_tmem = s[S_W_MMA_TMEM];
+  out->wait_epi_done = s[S_W_EPI_DONE]; out->mma_chunks = s[S_MMA_CHUNKS];
   return MK_OK;
 }
 
 int mk_counters_reset(mk_handle* h) {
   if (!h) return fail(MK_ERR_CONFIG, "null handle");
   CK(cudaSetDevice(h->device));
-  CK(cudaMemset(h->d_stats, 0, 16 * sizeof(unsigned long long)));
+  CK(cudaMemset(h->d_stats, 0, 32 * sizeof(unsigned long long)));
   return MK_OK;
 }
 
@@ -2747,6 +2917,7 @@ int mk_destroy(mk_handle* h) {
   cudaFree(h->d_mailbox); cudaFree(h->d_mb_head); cudaFree(h->d_mb_tail); cudaFree(h->d_die_of_sm);
   cudaFree(h->d_role_ctr); cudaFree(h->d_group_size); cudaFree(h->d_stats); cudaFree(h->d_err);
   cudaFree(h->d_log); cudaFree(h->d_log_cursor); cudaFree(h->d_tile_log); cudaFree(h->d_tile_cursor);
+  cudaFree(h->d_tmaps);
   if (h->h_err) cudaFreeHost(h->h_err);
   delete h;
   return MK_OK;
