@@ -181,8 +181,10 @@ typedef struct mk_attn_params {
   int32_t n_splits;    /* splits per row allocated (t_max / S)                */
   int32_t t_max;
   float eps, scale;
-  int32_t sub_splits;  /* warps sharing one (item, head): partial pieces per split */
-  int32_t pad;
+  int32_t sub_splits;  /* warps sharing one (item, head) -- or, on the
+                          tensor-core path, warps per item (1, 2, 4)        */
+  int32_t mma;         /* 1: tensor-core path (head_dim 128, 64-token splits,
+                          group <= 4; K/V rows chunk-swizzled)             */
 } mk_attn_params;
 
 typedef struct mk_silu_params {

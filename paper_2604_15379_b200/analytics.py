@@ -10,6 +10,8 @@ step time.
 
 from __future__ import annotations
 
+import os
+
 from .machine import MachineConfig, ModelConfig
 from .taskgraph import LINEAR_OPS, STANDARD_TILE_PROFILE, OpKind
 
@@ -83,7 +85,8 @@ def fit_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
     return out
 
 
-UMMA_MIN_BATCH = 16      # batch rows from which the tcgen05 body is used
+# batch rows from which the tcgen05 body is used (MK_UMMA_MIN_BATCH overrides)
+UMMA_MIN_BATCH = int(os.environ.get("MK_UMMA_MIN_BATCH", "4"))
 UMMA_MAX_TM = 64         # batch rows per tcgen05 m-tile (UMMA N, TMEM columns)
 
 

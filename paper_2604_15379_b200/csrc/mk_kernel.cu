@@ -158,6 +158,18 @@ struct SchedSmem {
 };
 
 constexpr size_t kRingOffset = (sizeof(Smem) + 1023) / 1024 * 1024;
+
+// Tensor-core split-KV attention (attn_mma_pass) applies to head_dim 128
+// with 64-token splits and up to 4 query heads per kv head.
+constexpr int kAttnHD = 128;
+constexpr int kAttnSplit = 64;
+constexpr int kAttnMaxG = 4;                   // query heads per kv head on this path
+
+__host__ __device__ __forceinline__ bool attn_mma_path(const mk_attn_params& p) {
+  return p.mma != 0 && p.head_dim == kAttnHD && p.split == kAttnSplit && p.group <= kAttnMaxG;
+}
+
+
 constexpr size_t kSmemBytes = kRingOffset + size_t(kSlots) * kSlotBytes;
 
 __device__ __forceinline__ bool aborted(const KArgs& a) {
@@ -443,12 +455,13 @@ struct SlotIter {
       bytes = bytes_kv; kv = 0; ++item;
       return true;
     }
+    const bool full = attn_mma_path(p);   // tensor-core path: whole 64-token blocks
     for (; item < ie; ++item) {
       const int b = item / p.n_splits, sp = item % p.n_splits;
       const int pos = p.positions[b];
       const int t0 = sp * p.split;
       if (t0 > pos) continue;
-      const int nc = min(p.split, pos - t0);
+      const int nc = full ? p.split : min(p.split, pos - t0);
       if (nc <= 0) continue;
       const size_t row = (size_t(b) * p.kv_heads + p.kv_head) * p.t_max + t0;
       src_k = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + row * p.head_dim;
@@ -1865,9 +1878,230 @@ __device__ void attn_pass(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core split-KV attention (head_dim 128, 64-token splits).  The K/V
+// cache rows are stored with their 16-byte chunks XOR-swizzled by
+// (token & 7), so the ring slots feed ldmatrix without bank conflicts.  A
+// pass holds 8 / wpi items (item = (row, split) of one kv head); wpi warps
+// share an item, each over 64 / wpi tokens:
+//   S[G heads x tokens] = Q K^T    mma.m16n8k16 (A rows = the G query heads)
+//   online softmax in registers     (quad shuffles, ex2, log2-domain max)
+//   O[G x 128] += P V               (P re-packed from the S fragments, V via
+//                                    ldmatrix.trans)
+// The warps of an item merge (m, l, o) through shared memory; the item's
+// first warp writes the split partial for the reduce task.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t kv_swz(int token, int chunk) {   // byte offset in a slot
+  return uint32_t(token * (kAttnHD * 2) + ((chunk ^ (token & 7)) << 4));
+}
+
+struct AttnMmaScratch {
+  uint16_t q[kConsWarps][kAttnMaxG][kAttnHD];  // per warp: normed + roped q of the group
+  float xch[kConsWarps][kAttnMaxG][kAttnHD + 4];  // per warp: (o[128], m, l) per head
+};
+static_assert(sizeof(AttnMmaScratch) <= size_t(kXsBytes), "attention scratch exceeds the union");
+
+__device__ void attn_mma_pass(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
+                              const mk_attn_params& p, int i0, int i1, int ct) {
+  const int G = p.group;
+  const int wpi = p.sub_splits;              // warps per item (1, 2 or 4)
+  const int tpw = kAttnSplit / wpi;          // tokens per warp
+  const int warp = ct >> 5, lane = ct & 31;
+  const int slot_item = warp / wpi, sw = warp % wpi;
+  const int g = lane >> 2, c = lane & 3;     // mma fragment row / column pair
+  AttnMmaScratch& sc = *reinterpret_cast<AttnMmaScratch*>(s.u.xs);
+
+  // items of the pass and their ring slots (K, V per active item)
+  int my_slot = -1, n_slots = 0, item = -1, pos = 0, t0 = 0;
+  for (int it = i0; it < i1; ++it) {
+    const int b = it / p.n_splits, sp = it % p.n_splits;
+    const int ps = p.positions[b];
+    const int tt0 = sp * kAttnSplit;
+    if (it - i0 == slot_item) { item = it; pos = ps; t0 = tt0; if (tt0 <= ps) my_slot = n_slots; }
+    if (tt0 <= ps) n_slots += 2;
+  }
+  const bool active = my_slot >= 0;
+  const int b = active ? item / p.n_splits : 0;
+  const int sp = active ? item % p.n_splits : 0;
+  const int nvalid = active ? min(kAttnSplit, pos + 1 - t0) : 0;   // incl. the new token
+  const int tok0 = sw * tpw;                                         // this warp's tokens
+  const bool trace = a.log != nullptr && ct == 0;
+  uint64_t ph0 = trace ? globaltimer() : 0, ph1 = ph0, ph2 = ph0;
+
+  float m_run = -INFINITY, l_run = 0.f;
+  float o[16][4];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) o[u][0] = o[u][1] = o[u][2] = o[u][3] = 0.f;
+
+  if (active && tok0 < nvalid) {
+    const uint16_t* qkv = reinterpret_cast<const uint16_t*>(p.qkv) + size_t(b) * p.ldqkv;
+    const float* cs = p.rope_cos + size_t(pos) * (kAttnHD / 2);
+    const float* sn = p.rope_sin + size_t(pos) * (kAttnHD / 2);
+    const int dl = lane & 15, half = lane >> 4;
+    // q_norm + RoPE of the item's G heads -> bf16 (unscaled, as the model's q)
+    for (int h = half; h < G; h += 2) {
+      float qv[8];
+      norm_rope8<kAttnHD>(qkv + (p.kv_head * G + h) * kAttnHD, reinterpret_cast<const uint16_t*>(p.q_gamma),
+                          p.eps, cs, sn, dl, qv);
+      uint4 pk;
+      pk.x = pack_bf16(qv[0], qv[1]); pk.y = pack_bf16(qv[2], qv[3]);
+      pk.z = pack_bf16(qv[4], qv[5]); pk.w = pack_bf16(qv[6], qv[7]);
+      *reinterpret_cast<uint4*>(&sc.q[warp][h][dl * 8]) = pk;
+    }
+    if (trace) ph1 = globaltimer();
+    Ring rk = r; rk.k += my_slot;
+    cons_wait_slot(a, s, rk);
+    uint8_t* kslot = ring + size_t(rk.k % kSlots) * kSlotBytes;
+    Ring rv = rk; ++rv.k;
+    cons_wait_slot(a, s, rv);
+    uint8_t* vslot = ring + size_t(rv.k % kSlots) * kSlotBytes;
+    if (trace) ph2 = globaltimer();
+    // the token being decoded: k_norm + RoPE and v from the qkv row, into
+    // the smem slots (and appended to the cache) by the warp that owns it
+    const int nt = pos - t0;
+    if (nt >= tok0 && nt < tok0 + tpw) {
+      float kn[8];
+      norm_rope8<kAttnHD>(qkv + p.q_heads * kAttnHD + p.kv_head * kAttnHD,
+                          reinterpret_cast<const uint16_t*>(p.k_gamma), p.eps, cs, sn, dl, kn);
+      uint4 kv4;
+      if (half == 0) {
+        kv4.x = pack_bf16(kn[0], kn[1]); kv4.y = pack_bf16(kn[2], kn[3]);
+        kv4.z = pack_bf16(kn[4], kn[5]); kv4.w = pack_bf16(kn[6], kn[7]);
+      } else {
+        kv4 = ldg128_cg(qkv + (p.q_heads + p.kv_heads) * kAttnHD + p.kv_head * kAttnHD + dl * 8);
+      }
+      const uint32_t off = kv_swz(nt, dl);
+      *reinterpret_cast<uint4*>((half == 0 ? kslot : vslot) + off) = kv4;
+      const size_t crow = ((size_t(b) * p.kv_heads + p.kv_head) * p.t_max + pos) * kAttnHD;
+      uint16_t* cache = reinterpret_cast<uint16_t*>(half == 0 ? p.k_cache : p.v_cache);
+      *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(cache + crow) + ((dl ^ (pos & 7)) << 4)) = kv4;
+    }
+    __syncwarp();
+    // Q fragments: row g = head g (g < G), 8 k-steps of 16 dims
+    uint32_t qa0[8], qa2[8];
+#pragma unroll
+    for (int st = 0; st < 8; ++st) {
+      qa0[st] = g < G ? *reinterpret_cast<const uint32_t*>(&sc.q[warp][g][16 * st + 2 * c]) : 0u;
+      qa2[st] = g < G ? *reinterpret_cast<const uint32_t*>(&sc.q[warp][g][16 * st + 8 + 2 * c]) : 0u;
+    }
+    const uint32_t ks = smem_u32(kslot), vs = smem_u32(vslot);
+    const float qscale = p.scale * 1.4426950408889634f;
+    // S = Q K^T over the warp's tokens, n-tile j = tokens tok0 + 8j ..
+    float sfr[8][2];
+    const int nj = tpw / 8;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sfr[j][0] = sfr[j][1] = -INFINITY;
+      if (j >= nj) continue;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const int tk = tok0 + 8 * j + (lane & 7);
+#pragma unroll
+      for (int st = 0; st < 8; st += 2) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(ks + kv_swz(tk, 2 * st + (lane >> 3)), b0, b1, b2, b3);
+        mma_bf16_16816(acc, qa0[st], qa2[st], b0, b1);
+        mma_bf16_16816(acc, qa0[st + 1], qa2[st + 1], b2, b3);
+      }
+      const int t_a = tok0 + 8 * j + 2 * c;
+      sfr[j][0] = t_a < nvalid ? acc[0] * qscale : -INFINITY;
+      sfr[j][1] = t_a + 1 < nvalid ? acc[1] * qscale : -INFINITY;
+    }
+    // softmax over the warp's tokens (row g spread over the lane quad)
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) mx = fmaxf(mx, fmaxf(sfr[j][0], sfr[j][1]));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    float lsum = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sfr[j][0] = mx == -INFINITY ? 0.f : ex2(sfr[j][0] - mx);
+      sfr[j][1] = mx == -INFINITY ? 0.f : ex2(sfr[j][1] - mx);
+      lsum += sfr[j][0] + sfr[j][1];
+    }
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
+    lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
+    m_run = mx; l_run = lsum;
+    // O = P V: k-step t = tokens tok0 + 16t .., n-tiles of 8 dims
+    const int nt16 = tpw / 16;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (t >= nt16) continue;
+      const uint32_t pa0 = pack_bf16(sfr[2 * t][0], sfr[2 * t][1]);
+      const uint32_t pa2 = pack_bf16(sfr[2 * t + 1][0], sfr[2 * t + 1][1]);
+      const int tv = tok0 + 16 * t + ((lane >> 3) & 1) * 8 + (lane & 7);
+#pragma unroll
+      for (int u = 0; u < 16; u += 2) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(vs + kv_swz(tv, u + (lane >> 4)), b0, b1, b2, b3);
+        mma_bf16_16816(o[u], pa0, pa2, b0, b1);
+        mma_bf16_16816(o[u + 1], pa0, pa2, b2, b3);
+      }
+    }
+  }
+  // release the item's K/V slots as soon as its warps are done (each of the
+  // wpi warps supplies 8 / wpi of the slot's 8 arrivals), so the fetch warp
+  // refills them with the next pass while this one merges
+  __syncwarp();
+  if (active && lane == 0) {
+    const uint32_t kpos = r.k + uint32_t(my_slot);
+    mbar_arrive_cnt(&s.empty[kpos % kSlots], uint32_t(kConsWarps / wpi));
+    mbar_arrive_cnt(&s.empty[(kpos + 1) % kSlots], uint32_t(kConsWarps / wpi));
+  }
+  r.k += uint32_t(n_slots);
+  const uint64_t ph3 = trace ? globaltimer() : 0;
+
+  // merge the item's warps; the first warp writes the split partial
+  if (wpi > 1) {
+    if (active && g < G) {
+      float* x = sc.xch[warp][g];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) { x[8 * u + 2 * c] = o[u][0]; x[8 * u + 2 * c + 1] = o[u][1]; }
+      if (c == 0) { x[kAttnHD] = m_run; x[kAttnHD + 1] = l_run; }
+    }
+    bar_sync(1, kCons);
+    if (active && sw == 0) {
+      for (int e = lane; e < G * kAttnHD; e += 32) {
+        const int h = e / kAttnHD, d = e % kAttnHD;
+        float M = -INFINITY;
+        for (int k = 0; k < wpi; ++k) M = fmaxf(M, sc.xch[warp + k][h][kAttnHD]);
+        float on = 0.f, ln = 0.f;
+        for (int k = 0; k < wpi; ++k) {
+          const float* x = sc.xch[warp + k][h];
+          const float f = M == -INFINITY ? 0.f : ex2(x[kAttnHD] - M);
+          on = fmaf(x[d], f, on);
+          ln = fmaf(x[kAttnHD + 1], f, ln);
+        }
+        float* dst = p.partial + (((size_t(b) * p.kv_heads + p.kv_head) * p.n_splits + sp) * G + h) * (kAttnHD + 4);
+        dst[d] = on;
+        if (d == 0) { dst[kAttnHD] = M; dst[kAttnHD + 1] = ln; }
+      }
+    }
+    bar_sync(1, kCons);              // xch / q staging reusable by the next pass
+    if (trace) {
+      phase_rec(a, 2, i0, ph0, ph1);     // prologue (q norm + rope)
+      phase_rec(a, 3, i0, ph1, ph2);     // waiting for the K/V slots
+      phase_rec(a, 4, i0, ph2, ph3);     // new token + QK / softmax / PV
+      phase_rec(a, 5, i0, ph3, globaltimer());   // merge + partial write
+    }
+  } else if (active && g < G) {
+    float* dst = p.partial + (((size_t(b) * p.kv_heads + p.kv_head) * p.n_splits + sp) * G + g) * (kAttnHD + 4);
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      *reinterpret_cast<float2*>(dst + 8 * u + 2 * c) = make_float2(o[u][0], o[u][1]);
+    if (c == 0) { dst[kAttnHD] = m_run; dst[kAttnHD + 1] = l_run; }
+  }
+}
+
 __device__ void run_attn_partial(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
                                  const mk_task& t, int ib, int ie, int ct) {
   const mk_attn_params& p = *P<mk_attn_params>(a, t);
+  if (attn_mma_path(p)) {                                  // tensor-core path
+    const int per = kConsWarps / p.sub_splits;
+    for (int i = ib; i < ie; i += per) attn_mma_pass(a, s, ring, r, p, i, min(ie, i + per), ct);
+    return;
+  }
   const int per = kConsWarps / (p.group * p.sub_splits);
   for (int i = ib; i < ie; i += per) {
     const int i1 = min(ie, i + per);
@@ -2607,10 +2841,13 @@ static int validate_graph(const mk_graph_desc* g) {
       const mk_attn_params* p = reinterpret_cast<const mk_attn_params*>(
           static_cast<const uint8_t*>(g->params) + t.param_off);
       const int hd = p->head_dim;
+      const bool mma = attn_mma_path(*p);
+      // tensor-core path: a pass's 2 * 8 / wpi K/V slots must fit the ring
+      const bool ws_ok = mma ? ((p->sub_splits == 2 || p->sub_splits == 4) && 2 * (kConsWarps / p->sub_splits) <= kSlots)
+                             : (p->group * p->sub_splits <= kConsWarps && kConsWarps % (p->group * p->sub_splits) == 0);
       if ((hd != 16 && hd != 32 && hd != 64 && hd != 128) || p->group < 1 || p->group > 8 ||
           8 % p->group || size_t(p->split) * hd * 2 > size_t(kSlotBytes) ||
-          p->n_splits > kMaxSplits || p->sub_splits < 1 || p->group * p->sub_splits > kConsWarps ||
-          kConsWarps % (p->group * p->sub_splits))
+          p->n_splits > kMaxSplits || p->sub_splits < 1 || !ws_ok || (mma && p->t_max % kAttnSplit))
         return fail(MK_ERR_CONFIG, "attention task " + std::to_string(i) + " has unsupported shapes");
     }
   }

@@ -27,6 +27,7 @@ tensor, and its output block starts at column ``x*N_local``.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 from . import _lib as L
@@ -45,6 +46,9 @@ def is_umma_tile(tile, fused: bool) -> bool:
 
 
 KSPLIT_MIN_BALANCE = 0.85
+# tensor-core attention from this batch on (measured: equal at 16, faster at
+# 64; the CUDA-core split path has the lower latency for 1-2 items per unit)
+ATTN_MMA_MIN_BATCH = int(os.environ.get("MK_ATTN_MMA_MIN_BATCH", "16"))
 
 
 def gemv_fast_shape(batch_rows: int, rows: int, t_k: int) -> bool:
@@ -79,6 +83,8 @@ class LoweringOptions:
                                    # activation staging when the rows fit
     bypass_noop: bool = True       # consumers of a fused (no-op) norm task wait
                                    # on that task's own predecessor event
+    attn_mma: bool = os.environ.get("MK_ATTN_MMA", "1") != "0"
+                                   # tensor-core split-KV attention (head_dim 128)
     ksplit: bool = True            # die tasks: K-split slot ranges per worker
                                    # instead of whole tiles
 
@@ -262,7 +268,15 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         p.eps, p.scale = spec.eps, hd ** -0.5
         # one item per unit (small batch): two warps share each (item, head)
         # and write two partial pieces; otherwise one warp per (item, head)
-        p.sub_splits = 2 if (B * bufs.n_splits <= u_attn and 8 % (2 * spec.group) == 0) else 1
+        if opts.attn_mma and hd == 128 and bufs.split == 64 and spec.group <= 4 \
+                and B >= ATTN_MMA_MIN_BATCH:
+            p.mma = 1
+            # tensor-core path (csrc attn_mma_pass): warps per item so that
+            # every consumer warp has work -- 8 / wpi items per pass, whose
+            # 2 * 8 / wpi K/V slots must fit the 10-slot ring (wpi >= 2)
+            p.sub_splits = int(os.environ.get("MK_ATTN_WPI", "2"))
+        else:
+            p.sub_splits = 2 if (B * bufs.n_splits <= u_attn and 8 % (2 * spec.group) == 0) else 1
         return blob.add(p)
 
     def gemm_tile_of(kind):

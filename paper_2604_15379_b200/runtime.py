@@ -127,6 +127,7 @@ def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
     hd = sp.head_dim
     split = split or max(8, 8192 // hd)
     n_splits = (t_max + split - 1) // split
+    t_max = n_splits * split          # whole splits: a split's K/V block never leaves its row
     st = DeviceState(sp, B, t_max, split, n_splits)
     w = weights.to(dev)
     tiles = _graph_tiles(g)
@@ -326,13 +327,15 @@ class Megakernel:
             pass
 
 
-def _default_lm_tile(spec: Qwen3Spec, batch: int, t_m: int | None = None):
+def _default_lm_tile(spec: Qwen3Spec, batch: int, t_m: int | None = None,
+                     umma: bool | None = None):
     """LM-head tile: the tcgen05 body (128 x 64, vocab padded to 256) from
     UMMA_MIN_BATCH rows on, else the warp-row GEMV rule of gemv_tiles."""
     if t_m is None:
-        t_m = default_t_m(batch)
+        t_m = default_t_m(batch) if umma is not False else 16
     rows = min(batch, t_m)
-    if rows >= UMMA_MIN_BATCH and spec.hidden % 64 == 0:
+    use = umma if umma is not None else rows >= UMMA_MIN_BATCH
+    if use and spec.hidden % 64 == 0:
         return (t_m, 128, 64)
     t_m = min(t_m, 16)
     t_n = 16 if rows <= 4 else 32

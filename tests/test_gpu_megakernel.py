@@ -264,7 +264,7 @@ def test_watchdog_reports_deadlock(topo, machine):
     lib.mk_destroy(h)
 
 
-def _mini(machine, mode, B, layers=2, t_m=None):
+def _mini(machine, mode, B, layers=2, t_m=None, umma=None):
     """Qwen3-shaped mini model whose widths divide the 128-row tcgen05 tiles."""
     from paper_2604_15379_b200 import build_decoder_layer
     from paper_2604_15379_b200.analytics import device_tiles
@@ -274,7 +274,7 @@ def _mini(machine, mode, B, layers=2, t_m=None):
                     dtype_bytes=2)
     spec = Qwen3Spec(512, 1024, layers, 4, 2, 128, 1024)
     g = build_decoder_layer(m, machine, mode, B,
-                            tile_overrides=device_tiles(m, machine, mode, B, t_m=t_m),
+                            tile_overrides=device_tiles(m, machine, mode, B, t_m=t_m, umma=umma),
                             layers=layers)
     return g, spec
 
@@ -284,11 +284,12 @@ def _mini(machine, mode, B, layers=2, t_m=None):
 def test_gemv_ksplit_decode_matches_oracle(topo, machine, B, ksplit):
     """CUDA-core GEMV body (B <= 8) on the mini model: K-chunks per tile > 1,
     so the K-split ranges cut tiles into pieces."""
-    from paper_2604_15379_b200.runtime import Megakernel
+    from paper_2604_15379_b200.runtime import Megakernel, _default_lm_tile
     from paper_2604_15379_b200.weights import Qwen3Weights
-    g, spec = _mini(machine, "chiplet", B)
+    g, spec = _mini(machine, "chiplet", B, umma=False)
     w = Qwen3Weights.random(spec, seed=32)
-    mk = Megakernel(g, w, t_max=40, topo=topo, ksplit=ksplit, watchdog_s=5.0)
+    mk = Megakernel(g, w, t_max=40, topo=topo, ksplit=ksplit, watchdog_s=5.0,
+                    lm_tile=_default_lm_tile(spec, B, umma=False))
     worst, _ = _decode_vs_oracle(mk, w, B, steps=6, t_max=40)
     mk.close()
     assert worst < RTOL
@@ -359,7 +360,8 @@ def test_ksplit_segments_cover_every_slot_once(topo, machine, dist):
 
 
 @pytest.mark.parametrize("mode,sched", [("chiplet", "per_die"), ("standard", "flat")])
-@pytest.mark.parametrize("B,dist,t_m,ksplit", [(16, "m_tile", None, True),
+@pytest.mark.parametrize("B,dist,t_m,ksplit", [(4, "m_tile", None, True),
+                                               (16, "m_tile", None, True),
                                                (32, "m_tile", None, True),
                                                (48, "m_split", None, True),
                                                (64, "m_tile", None, True),

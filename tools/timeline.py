@@ -46,9 +46,10 @@ def main():
     exe = [r for r in recs if r.kind == 1]
     phases = {}
     for r in recs:
-        if r.kind in (2, 3, 4):
+        if r.kind in (2, 3, 4, 5):
             phases.setdefault(r.kind, []).append((r.t_end - r.t_start) / 1e3)
-    for k, name in ((2, "attn prologue"), (3, "attn K/V slot wait"), (4, "attn token loop")):
+    for k, name in ((2, "attn prologue"), (3, "attn K/V slot wait"), (4, "attn token loop"),
+                    (5, "attn merge")):
         v = phases.get(k, [])
         if v:
             v.sort()
