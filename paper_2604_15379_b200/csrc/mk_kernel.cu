@@ -126,6 +126,7 @@ struct AttnScratch {
 struct Smem {
   uint64_t full[kSlots];
   uint64_t empty[kSlots];
+  uint32_t slot_tag[kSlots];        // ring position last loaded into each slot
   uint64_t tq_full[kTQ];
   uint64_t tq_empty[kTQ];
   int4 tq[kTQ];
@@ -1902,39 +1903,33 @@ struct AttnMmaScratch {
 };
 static_assert(sizeof(AttnMmaScratch) <= size_t(kXsBytes), "attention scratch exceeds the union");
 
-__device__ void attn_mma_pass(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
-                              const mk_attn_params& p, int i0, int i1, int ct) {
-  const int G = p.group;
-  const int wpi = p.sub_splits;              // warps per item (1, 2 or 4)
-  const int tpw = kAttnSplit / wpi;          // tokens per warp
-  const int warp = ct >> 5, lane = ct & 31;
-  const int slot_item = warp / wpi, sw = warp % wpi;
-  const int g = lane >> 2, c = lane & 3;     // mma fragment row / column pair
-  AttnMmaScratch& sc = *reinterpret_cast<AttnMmaScratch*>(s.u.xs);
-
-  // items of the pass and their ring slots (K, V per active item)
-  int my_slot = -1, n_slots = 0, item = -1, pos = 0, t0 = 0;
-  for (int it = i0; it < i1; ++it) {
-    const int b = it / p.n_splits, sp = it % p.n_splits;
-    const int ps = p.positions[b];
-    const int tt0 = sp * kAttnSplit;
-    if (it - i0 == slot_item) { item = it; pos = ps; t0 = tt0; if (tt0 <= ps) my_slot = n_slots; }
-    if (tt0 <= ps) n_slots += 2;
+// Wait for ring position kpos.  Barrier-free warps may wait more than one
+// ring lap ahead of the fill, where the mbarrier parity aliases: they also
+// require the fetch warp's position tag of the slot to match.
+__device__ __forceinline__ void attn_wait_slot(const KArgs& a, Smem& s, uint32_t kpos, bool tagged) {
+  const int i = int(kpos % kSlots);
+  const uint32_t par = (kpos / kSlots) & 1;
+  if (!tagged) { mbar_wait(a, &s.full[i], par, -3); return; }
+  Spin sp;
+  for (;;) {
+    if (*reinterpret_cast<volatile uint32_t*>(&s.slot_tag[i]) == kpos && mbar_test_wait(&s.full[i], par)) return;
+    if (!sp.ok(a, -3)) return;
   }
-  const bool active = my_slot >= 0;
-  const int b = active ? item / p.n_splits : 0;
-  const int sp = active ? item % p.n_splits : 0;
-  const int nvalid = active ? min(kAttnSplit, pos + 1 - t0) : 0;   // incl. the new token
-  const int tok0 = sw * tpw;                                         // this warp's tokens
-  const bool trace = a.log != nullptr && ct == 0;
-  uint64_t ph0 = trace ? globaltimer() : 0, ph1 = ph0, ph2 = ph0;
+}
 
-  float m_run = -INFINITY, l_run = 0.f;
-  float o[16][4];
-#pragma unroll
-  for (int u = 0; u < 16; ++u) o[u][0] = o[u][1] = o[u][2] = o[u][3] = 0.f;
-
-  if (active && tok0 < nvalid) {
+// One warp's tokens [tok0, tok0 + tpw) of item (b, split at t0): q_norm +
+// RoPE of the group's heads, K/V slots at ring positions kpos, kpos + 1, the
+// decoded token folded into the slots (and appended to the cache), then
+// S = Q K^T, online softmax and O = P V in registers.
+__device__ __forceinline__ void attn_mma_tokens(const KArgs& a, Smem& s, uint8_t* ring,
+                                                const mk_attn_params& p, int b, int pos, int t0,
+                                                int nvalid, int tok0, int tpw, uint32_t kpos,
+                                                bool tagged, int warp, int lane,
+                                                float (&o)[16][4], float& m_run, float& l_run,
+                                                bool trace, uint64_t& ph1, uint64_t& ph2) {
+  const int G = p.group;
+  const int g = lane >> 2, c = lane & 3;
+  AttnMmaScratch& sc = *reinterpret_cast<AttnMmaScratch*>(s.u.xs);
     const uint16_t* qkv = reinterpret_cast<const uint16_t*>(p.qkv) + size_t(b) * p.ldqkv;
     const float* cs = p.rope_cos + size_t(pos) * (kAttnHD / 2);
     const float* sn = p.rope_sin + size_t(pos) * (kAttnHD / 2);
@@ -1950,12 +1945,10 @@ __device__ void attn_mma_pass(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
       *reinterpret_cast<uint4*>(&sc.q[warp][h][dl * 8]) = pk;
     }
     if (trace) ph1 = globaltimer();
-    Ring rk = r; rk.k += my_slot;
-    cons_wait_slot(a, s, rk);
-    uint8_t* kslot = ring + size_t(rk.k % kSlots) * kSlotBytes;
-    Ring rv = rk; ++rv.k;
-    cons_wait_slot(a, s, rv);
-    uint8_t* vslot = ring + size_t(rv.k % kSlots) * kSlotBytes;
+    attn_wait_slot(a, s, kpos, tagged);
+    attn_wait_slot(a, s, kpos + 1, tagged);
+    uint8_t* kslot = ring + size_t(kpos % kSlots) * kSlotBytes;
+    uint8_t* vslot = ring + size_t((kpos + 1) % kSlots) * kSlotBytes;
     if (trace) ph2 = globaltimer();
     // the token being decoded: k_norm + RoPE and v from the qkv row, into
     // the smem slots (and appended to the cache) by the warp that owns it
@@ -2039,7 +2032,43 @@ __device__ void attn_mma_pass(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
         mma_bf16_16816(o[u + 1], pa0, pa2, b2, b3);
       }
     }
+}
+
+__device__ void attn_mma_pass(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
+                              const mk_attn_params& p, int i0, int i1, int ct) {
+  const int G = p.group;
+  const int wpi = p.sub_splits;              // warps per item (1, 2 or 4)
+  const int tpw = kAttnSplit / wpi;          // tokens per warp
+  const int warp = ct >> 5, lane = ct & 31;
+  const int slot_item = warp / wpi, sw = warp % wpi;
+  const int g = lane >> 2, c = lane & 3;     // mma fragment row / column pair
+  AttnMmaScratch& sc = *reinterpret_cast<AttnMmaScratch*>(s.u.xs);
+
+  // items of the pass and their ring slots (K, V per active item)
+  int my_slot = -1, n_slots = 0, item = -1, pos = 0, t0 = 0;
+  for (int it = i0; it < i1; ++it) {
+    const int b = it / p.n_splits, sp = it % p.n_splits;
+    const int ps = p.positions[b];
+    const int tt0 = sp * kAttnSplit;
+    if (it - i0 == slot_item) { item = it; pos = ps; t0 = tt0; if (tt0 <= ps) my_slot = n_slots; }
+    if (tt0 <= ps) n_slots += 2;
   }
+  const bool active = my_slot >= 0;
+  const int b = active ? item / p.n_splits : 0;
+  const int sp = active ? item % p.n_splits : 0;
+  const int nvalid = active ? min(kAttnSplit, pos + 1 - t0) : 0;   // incl. the new token
+  const int tok0 = sw * tpw;                                         // this warp's tokens
+  const bool trace = a.log != nullptr && ct == 0;
+  uint64_t ph0 = trace ? globaltimer() : 0, ph1 = ph0, ph2 = ph0;
+
+  float m_run = -INFINITY, l_run = 0.f;
+  float o[16][4];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) o[u][0] = o[u][1] = o[u][2] = o[u][3] = 0.f;
+
+  if (active && tok0 < nvalid)
+    attn_mma_tokens(a, s, ring, p, b, pos, t0, nvalid, tok0, tpw, r.k + uint32_t(my_slot), false,
+                    warp, lane, o, m_run, l_run, trace, ph1, ph2);
   // release the item's K/V slots as soon as its warps are done (each of the
   // wpi warps supplies 8 / wpi of the slot's 8 arrivals), so the fetch warp
   // refills them with the next pass while this one merges
@@ -2094,10 +2123,63 @@ __device__ void attn_mma_pass(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   }
 }
 
+// Barrier-free variant (one warp per item, wpi = 1): warp w takes the unit's
+// items w, w + 8, ...; each warp waits only for its own item's K/V slots
+// (tag-checked: it may run more than a ring lap ahead), releases them with
+// all 8 arrivals as soon as it is done and writes its split partial -- no
+// pass barrier, no cross-warp merge, the fetch warp streams continuously.
+__device__ void attn_mma_free(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
+                              const mk_attn_params& p, int ib, int ie, int ct) {
+  const int G = p.group;
+  const int warp = ct >> 5, lane = ct & 31;
+  const int g = lane >> 2, c = lane & 3;
+  const uint32_t base = r.k;
+  uint32_t act = 0;                          // active items before the current one
+  int last_b = -1, pos = 0;
+  const bool trace = a.log != nullptr && lane == 0 && warp == 0;
+  for (int it = ib; it < ie; ++it) {
+    const int b = it / p.n_splits, sp = it % p.n_splits;
+    if (b != last_b) { pos = p.positions[b]; last_b = b; }
+    const int t0 = sp * kAttnSplit;
+    if (t0 > pos) continue;
+    const uint32_t kpos = base + 2 * act;
+    ++act;
+    if (((it - ib) & (kConsWarps - 1)) != warp) continue;
+    uint64_t ph0 = trace ? globaltimer() : 0, ph1 = ph0, ph2 = ph0;
+    float m_run = -INFINITY, l_run = 0.f;
+    float o[16][4];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) o[u][0] = o[u][1] = o[u][2] = o[u][3] = 0.f;
+    const int nvalid = min(kAttnSplit, pos + 1 - t0);
+    attn_mma_tokens(a, s, ring, p, b, pos, t0, nvalid, 0, kAttnSplit, kpos, true, warp, lane,
+                    o, m_run, l_run, trace, ph1, ph2);
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive_cnt(&s.empty[kpos % kSlots], kConsWarps);
+      mbar_arrive_cnt(&s.empty[(kpos + 1) % kSlots], kConsWarps);
+    }
+    if (g < G) {
+      float* dst = p.partial + (((size_t(b) * p.kv_heads + p.kv_head) * p.n_splits + sp) * G + g) * (kAttnHD + 4);
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        *reinterpret_cast<float2*>(dst + 8 * u + 2 * c) = make_float2(o[u][0], o[u][1]);
+      if (c == 0) { dst[kAttnHD] = m_run; dst[kAttnHD + 1] = l_run; }
+    }
+    if (trace) {
+      const uint64_t ph3 = globaltimer();
+      phase_rec(a, 2, it, ph0, ph1);
+      phase_rec(a, 3, it, ph1, ph2);
+      phase_rec(a, 4, it, ph2, ph3);
+    }
+  }
+  r.k = base + 2 * act;
+}
+
 __device__ void run_attn_partial(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
                                  const mk_task& t, int ib, int ie, int ct) {
   const mk_attn_params& p = *P<mk_attn_params>(a, t);
   if (attn_mma_path(p)) {                                  // tensor-core path
+    if (p.sub_splits == 1) { attn_mma_free(a, s, ring, r, p, ib, ie, ct); return; }
     const int per = kConsWarps / p.sub_splits;
     for (int i = ib; i < ie; i += per) attn_mma_pass(a, s, ring, r, p, i, min(ie, i + per), ct);
     return;
@@ -2338,6 +2420,7 @@ __device__ void ring_warp(const KArgs& a, Smem& s, uint8_t* ring, int worker) {
   const uint64_t pol = policy_evict_first();
   int si = 0;                       // ring slot index / phase
   uint32_t sph = 0;
+  uint32_t pos_k = 0;               // ring position (= the consumers' Ring::k)
   unsigned long long w_empty = 0;
   struct Flush {
     const KArgs& a; unsigned long long& e;
@@ -2354,6 +2437,7 @@ __device__ void ring_warp(const KArgs& a, Smem& s, uint8_t* ring, int worker) {
     uint32_t bytes;
     while (it.next(a, src, bytes)) {
       if (!mbar_wait_p(a, &s.empty[si], sph ^ 1, -2, w_empty)) return;
+      *reinterpret_cast<volatile uint32_t*>(&s.slot_tag[si]) = pos_k++;
       if (a.debug & 2) {
         mbar_arrive(&s.full[si]);
       } else {
@@ -2483,7 +2567,7 @@ __global__ void __launch_bounds__(kThreads, 1) megakernel(const __grid_constant_
     const int rank = int(raw - (a.epoch - 1) * uint32_t(a.group_size[g]));
     role[0] = g;
     role[1] = rank;
-    for (int i = 0; i < kSlots; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], kConsWarps); }
+    for (int i = 0; i < kSlots; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], kConsWarps); s.slot_tag[i] = 0xffffffffu; }
     for (int i = 0; i < kTQ; ++i) { mbar_init(&s.tq_full[i], 1); mbar_init(&s.tq_empty[i], 1); }
     for (int i = 0; i < kXStagesMax; ++i) { mbar_init(&s.xfull[i], 1); mbar_init(&s.xempty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&s.tile_done[i], 1); mbar_init(&s.tmem_free[i], kConsWarps); }
@@ -2843,7 +2927,8 @@ static int validate_graph(const mk_graph_desc* g) {
       const int hd = p->head_dim;
       const bool mma = attn_mma_path(*p);
       // tensor-core path: a pass's 2 * 8 / wpi K/V slots must fit the ring
-      const bool ws_ok = mma ? ((p->sub_splits == 2 || p->sub_splits == 4) && 2 * (kConsWarps / p->sub_splits) <= kSlots)
+      const bool ws_ok = mma ? (p->sub_splits == 1 ||   // barrier-free warps
+                                ((p->sub_splits == 2 || p->sub_splits == 4) && 2 * (kConsWarps / p->sub_splits) <= kSlots))
                              : (p->group * p->sub_splits <= kConsWarps && kConsWarps % (p->group * p->sub_splits) == 0);
       if ((hd != 16 && hd != 32 && hd != 64 && hd != 128) || p->group < 1 || p->group > 8 ||
           8 % p->group || size_t(p->split) * hd * 2 > size_t(kSlotBytes) ||

@@ -46,9 +46,9 @@ def is_umma_tile(tile, fused: bool) -> bool:
 
 
 KSPLIT_MIN_BALANCE = 0.85
-# tensor-core attention from this batch on (measured: equal at 16, faster at
-# 64; the CUDA-core split path has the lower latency for 1-2 items per unit)
-ATTN_MMA_MIN_BATCH = int(os.environ.get("MK_ATTN_MMA_MIN_BATCH", "16"))
+# tensor-core attention from this batch on (barrier-free warps: measured
+# faster than the CUDA-core split path at every batch 1-64)
+ATTN_MMA_MIN_BATCH = int(os.environ.get("MK_ATTN_MMA_MIN_BATCH", "1"))
 
 
 def gemv_fast_shape(batch_rows: int, rows: int, t_k: int) -> bool:
@@ -274,7 +274,7 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
             # tensor-core path (csrc attn_mma_pass): warps per item so that
             # every consumer warp has work -- 8 / wpi items per pass, whose
             # 2 * 8 / wpi K/V slots must fit the 10-slot ring (wpi >= 2)
-            p.sub_splits = int(os.environ.get("MK_ATTN_WPI", "2"))
+            p.sub_splits = int(os.environ.get("MK_ATTN_WPI", "1"))
         else:
             p.sub_splits = 2 if (B * bufs.n_splits <= u_attn and 8 % (2 * spec.group) == 0) else 1
         return blob.add(p)
