@@ -271,6 +271,10 @@ int64_t mk_log_read(mk_handle* h, mk_log_rec* out, int64_t max_records);
 int mk_tile_log_enable(mk_handle* h, int64_t capacity);
 int64_t mk_tile_log_read(mk_handle* h, int32_t* out4, int64_t max_records);
 int mk_set_watchdog(mk_handle* h, double seconds);
+/* L2 prefetch run-ahead of each worker (CUDA-core kernel instance), in
+ * 16 KiB ring slots beyond the fetch warp (0 = off): weight slots of queued
+ * GEMM units are prefetched into L2 while the worker waits on dependencies. */
+int mk_set_prefetch(mk_handle* h, int slots);
 /* Diagnostics only: bit0 = consumers skip GEMM math, bit1 = no TMA copies,
  * bit2 = count wait cycles (mk_counters wait_*). */
 int mk_set_debug(mk_handle* h, int flags);

@@ -130,6 +130,7 @@ def load() -> C.CDLL:
     lib.mk_create.argtypes = [C.c_int, C.POINTER(GraphDesc), C.POINTER(Topology),
                               C.POINTER(C.c_void_p)]
     lib.mk_step.argtypes = [C.c_void_p, C.c_void_p]
+    lib.mk_set_prefetch.argtypes = [C.c_void_p, C.c_int]
     lib.mk_sync.argtypes = [C.c_void_p]
     lib.mk_counters_get.argtypes = [C.c_void_p, C.POINTER(Counters)]
     lib.mk_counters_reset.argtypes = [C.c_void_p]

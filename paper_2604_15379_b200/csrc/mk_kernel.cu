@@ -117,6 +117,7 @@ struct KArgs {
   const CUtensorMap* tmaps; // [n_tasks]: activation (x) tensor map of each tcgen05 GEMM task
   int x_stages;            // x ring stages (kXsBytes / x_stage_bytes, <= kXStagesMax)
   int x_stage_bytes;       // 128 * max NT over the graph's tcgen05 tasks
+  int pf_slots;            // L2 prefetch run-ahead of the prefetch warp (16 KiB slots)
 };
 
 struct AttnScratch {
@@ -140,6 +141,7 @@ struct Smem {
   int abort_flag;
   int piece_last;                   // K-split: this CTA summed the tile's pieces (GEMV)
   int epi_last;                     // K-split: same, tcgen05 epilogue warps
+  uint32_t ring_pos;                // slots the fetch warp has issued (prefetch warp's bound)
   // tcgen05 path
   uint64_t xfull[kXStagesMax], xempty[kXStagesMax];
   uint64_t tile_done[2], tmem_free[2];
@@ -2414,6 +2416,47 @@ __device__ void mailbox_warp(const KArgs& a, Smem& s, int g, int worker) {
   }
 }
 
+// L2 prefetch warp (warp 3 of the CUDA-core instance, where it is otherwise
+// idle): walks the same slot sequence as the fetch warp over the units
+// already queued in tq and issues cp.async.bulk.prefetch.L2 for up to
+// pf_slots slots beyond the fetch warp's position -- the weights (immutable
+// during the step) keep streaming from HBM while the ring is full and the
+// die waits on a dependency (attention, norms, the next event).
+template <int F>
+__device__ void prefetch_warp(const KArgs& a, Smem& s, int worker) {
+  if ((threadIdx.x & 31) != 0 || a.pf_slots <= 0) return;
+  uint32_t my_pos = 0;
+  for (uint32_t q = 0;; ++q) {
+    const int qi = q % kTQ;
+    {   // the unit is queued (no parity aliasing: q never passes the fill)
+      Spin sp;
+      bool ok = true;
+      while (!mbar_test_wait(&s.tq_full[qi], (q / kTQ) & 1)) {
+        if (!sp.ok(a, -16)) { ok = false; break; }
+        __nanosleep(128);
+      }
+      if (!ok) return;
+    }
+    const int4 ent = s.tq[qi];
+    if (ent.x < 0) return;
+    SlotIter<F> it;
+    it.init(a, a.tasks[ent.x], ent.y, ent.z, worker);
+    const bool gemm = a.tasks[ent.x].op == MK_OP_GEMM;
+    const void* src;
+    uint32_t bytes;
+    while (it.next(a, src, bytes)) {
+      Spin sp;
+      while (int32_t(my_pos - *reinterpret_cast<volatile uint32_t*>(&s.ring_pos)) >= a.pf_slots) {
+        if (!sp.ok(a, -16)) return;
+        __nanosleep(64);
+      }
+      if (gemm && int32_t(my_pos - *reinterpret_cast<volatile uint32_t*>(&s.ring_pos)) >= kSlots)
+        prefetch_l2(src, bytes);          // slots inside the ring window are being copied anyway
+      ++my_pos;
+    }
+  }
+}
+
 template <int F>
 __device__ void ring_warp(const KArgs& a, Smem& s, uint8_t* ring, int worker) {
   if ((threadIdx.x & 31) != 0) return;
@@ -2438,6 +2481,7 @@ __device__ void ring_warp(const KArgs& a, Smem& s, uint8_t* ring, int worker) {
     while (it.next(a, src, bytes)) {
       if (!mbar_wait_p(a, &s.empty[si], sph ^ 1, -2, w_empty)) return;
       *reinterpret_cast<volatile uint32_t*>(&s.slot_tag[si]) = pos_k++;
+      *reinterpret_cast<volatile uint32_t*>(&s.ring_pos) = pos_k;
       if (a.debug & 2) {
         mbar_arrive(&s.full[si]);
       } else {
@@ -2568,6 +2612,7 @@ __global__ void __launch_bounds__(kThreads, 1) megakernel(const __grid_constant_
     role[0] = g;
     role[1] = rank;
     for (int i = 0; i < kSlots; ++i) { mbar_init(&s.full[i], 1); mbar_init(&s.empty[i], kConsWarps); s.slot_tag[i] = 0xffffffffu; }
+    s.ring_pos = 0;
     for (int i = 0; i < kTQ; ++i) { mbar_init(&s.tq_full[i], 1); mbar_init(&s.tq_empty[i], 1); }
     for (int i = 0; i < kXStagesMax; ++i) { mbar_init(&s.xfull[i], 1); mbar_init(&s.xempty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&s.tile_done[i], 1); mbar_init(&s.tmem_free[i], kConsWarps); }
@@ -2611,6 +2656,8 @@ __global__ void __launch_bounds__(kThreads, 1) megakernel(const __grid_constant_
       }
     } else if (a.use_umma) {
       if constexpr ((F & kFeatUmma) != 0) xload_warp(a, s);
+    } else if (threadIdx.x >= 96) {
+      if constexpr ((F & kFeatUmma) == 0) prefetch_warp<F>(a, s, worker);
     }
   } else {
     if constexpr ((F & kFeatUmma) != 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(kConsRegsUmma));
@@ -2690,6 +2737,7 @@ struct mk_handle {
   const void* kernel = nullptr;
   CUtensorMap* d_tmaps = nullptr; // x tensor map per task (tcgen05 GEMMs)
   int x_stages = 1, x_stage_bytes = 2048;
+  int pf_slots = 0;             // L2 prefetch run-ahead per worker (mk_set_prefetch)
   // device buffers
   mk_task* d_tasks = nullptr;
   mk_unit* d_units = nullptr;
@@ -3130,6 +3178,7 @@ int mk_step(mk_handle* h, void* stream) {
   a.tmaps = h->d_tmaps;
   a.x_stages = h->x_stages;
   a.x_stage_bytes = h->x_stage_bytes;
+  a.pf_slots = h->pf_slots;
   void* args[] = {&a};
   CK(cudaLaunchCooperativeKernel(h->kernel, dim3(h->num_sms), dim3(kThreads), args,
                                  kSmemBytes, static_cast<cudaStream_t>(stream)));
@@ -3222,6 +3271,12 @@ int64_t mk_tile_log_read(mk_handle* h, int32_t* out4, int64_t max_records) {
 int mk_set_watchdog(mk_handle* h, double seconds) {
   if (!h || !(seconds > 0)) return fail(MK_ERR_CONFIG, "bad watchdog");
   h->watchdog_s = seconds;
+  return MK_OK;
+}
+
+int mk_set_prefetch(mk_handle* h, int slots) {
+  if (!h || slots < 0 || slots > 1024) return fail(MK_ERR_CONFIG, "bad prefetch depth");
+  h->pf_slots = slots;
   return MK_OK;
 }
 

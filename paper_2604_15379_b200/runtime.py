@@ -23,6 +23,7 @@ There is no CPU path: constructing a Megakernel without a GPU or without
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -246,6 +247,7 @@ class Megakernel:
                                    C.byref(h)))
         self.h = h
         L.check(self.lib.mk_set_watchdog(self.h, watchdog_s))
+        L.check(self.lib.mk_set_prefetch(self.h, int(os.environ.get("MK_PREFETCH", "0"))))
         self.steps = 0
 
     # ---- state -----------------------------------------------------------
