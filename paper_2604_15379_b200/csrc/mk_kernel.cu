@@ -1217,6 +1217,7 @@ __device__ void xload_warp(const KArgs& a, Smem& s) {
   const int xs_shift = __ffs(XS) - 1;
   const uint32_t XB = uint32_t(a.x_stage_bytes);
   uint32_t xs_load = 0, jq = 0;
+  const bool no_tma = (a.debug & 16) != 0;
   for (;;) {
     if (!mbar_wait(a, &s.job_full, jq & 1, -15)) break;
     ++jq;
@@ -1237,7 +1238,7 @@ __device__ void xload_warp(const KArgs& a, Smem& s) {
         const int xl = int(xs_load & uint32_t(XS - 1));
         if (!mbar_spin(a, &s.xempty[xl], ((xs_load >> xs_shift) & 1) ^ 1, -13)) return;
         if (leader) {
-          if (a.debug & 16) {          // diagnostics: no activation TMA
+          if (no_tma) {                // diagnostics: no activation TMA
             mbar_arrive(&s.xfull[xl]);
           } else {
             mbar_arrive_expect_tx(&s.xfull[xl], x_bytes);
@@ -1263,6 +1264,8 @@ __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
   int ri = 0; uint32_t rph = 0;              // ring slot index / phase
   uint32_t xs_mma = 0, tb_k = 0, jq = 0;
   unsigned long long w_full = 0, w_x = 0, w_tmem = 0, n_chunks = 0;
+  // diagnostics flags read once: the per-chunk path paces the die task
+  const bool prof = (a.debug & 4) != 0, no_mma = (a.debug & 8) != 0;
   const uint64_t adesc0 = umma_desc_sw128(smem_u32(ring));
   const uint64_t bdesc0 = umma_desc_sw128(smem_u32(s.u.xs));
   for (;;) {
@@ -1280,17 +1283,23 @@ __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
     Seg sg;
     while (it.next(sg)) {
       const int buf = tb_k & 1;
-      if (!mbar_wait_p(a, &s.tmem_free[buf], ((tb_k >> 1) & 1) ^ 1, -10, w_tmem)) return;
+      if (!(prof ? mbar_wait_p(a, &s.tmem_free[buf], ((tb_k >> 1) & 1) ^ 1, -10, w_tmem)
+                 : mbar_spin(a, &s.tmem_free[buf], ((tb_k >> 1) & 1) ^ 1, -10))) return;
       tc_fence_after();
       const uint32_t d = s.tmem_base + uint32_t(buf * 64);
       for (int c = sg.c0; c < sg.c1; ++c) {
-        ++n_chunks;
+        if (prof) ++n_chunks;
         const int xi = int(xs_mma & uint32_t(XS - 1));
-        if (!mbar_wait_p(a, &s.full[ri], rph, -11, w_full)) return;
-        if (!mbar_wait_p(a, &s.xfull[xi], (xs_mma >> xs_shift) & 1, -12, w_x)) return;
+        if (prof) {
+          if (!mbar_wait_p(a, &s.full[ri], rph, -11, w_full)) return;
+          if (!mbar_wait_p(a, &s.xfull[xi], (xs_mma >> xs_shift) & 1, -12, w_x)) return;
+        } else {
+          if (!mbar_spin(a, &s.full[ri], rph, -11)) return;
+          if (!mbar_spin(a, &s.xfull[xi], (xs_mma >> xs_shift) & 1, -12)) return;
+        }
         tc_fence_after();
         if (leader) {
-          if (a.debug & 8) {             // diagnostics: no MMA, release at once
+          if (no_mma) {                  // diagnostics: no MMA, release at once
             mbar_arrive_cnt(&s.empty[ri], kConsWarps);
             mbar_arrive(&s.xempty[xi]);
           } else {
@@ -1311,14 +1320,14 @@ __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
         ++xs_mma;
       }
       if (leader) {
-        if (a.debug & 8) mbar_arrive(&s.tile_done[buf]);
+        if (no_mma) mbar_arrive(&s.tile_done[buf]);
         else umma_commit(&s.tile_done[buf]);
       }
       __syncwarp();
       ++tb_k;
     }
   }
-  if (leader && (a.debug & 4)) {
+  if (leader && prof) {
     atomicAdd(&a.stats[S_W_MMA_FULL], w_full); atomicAdd(&a.stats[S_W_MMA_X], w_x);
     atomicAdd(&a.stats[S_W_MMA_TMEM], w_tmem); atomicAdd(&a.stats[S_MMA_CHUNKS], n_chunks);
   }
