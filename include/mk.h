@@ -185,6 +185,10 @@ typedef struct mk_attn_params {
                           tensor-core path, warps per item (1, 2, 4)        */
   int32_t mma;         /* 1: tensor-core path (head_dim 128, 64-token splits,
                           group <= 4; K/V rows chunk-swizzled)             */
+  int32_t fuse_reduce; /* 1: ATTN_PARTIAL: the last split of a row merges all
+                          splits into `out` (per-row arrival counters at
+                          red_ctr0); ATTN_REDUCE: no-op                    */
+  int32_t red_ctr0;    /* first per-row arrival sub-counter                 */
 } mk_attn_params;
 
 typedef struct mk_silu_params {

@@ -2134,6 +2134,69 @@ __device__ void attn_mma_pass(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   }
 }
 
+// Merge every split partial of row b (this kv head's G query heads) into
+// the attention output -- run by the warp whose split arrived last (the
+// ATTN_REDUCE stage folded into ATTN_PARTIAL).  Lane l owns dims 4l..4l+3.
+__device__ void attn_merge_row(const mk_attn_params& p, int b, int nsp, int lane) {
+  const int G = p.group;
+  const int stride = G * (kAttnHD + 4);
+  const float* base = p.partial + (size_t(b) * p.kv_heads + p.kv_head) * p.n_splits * stride;
+  uint16_t* out = reinterpret_cast<uint16_t*>(p.out);
+  constexpr int kB = 8;
+  for (int h = 0; h < G; ++h) {
+    const float* hb = base + h * (kAttnHD + 4);
+    float M = -INFINITY, den = 0.f;
+    float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < nsp; s0 += kB) {
+      float mv[kB], lv[kB];
+      float4 ov[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const bool ok = s0 + u < nsp;
+        const float* x = hb + size_t(s0 + u) * stride;
+        mv[u] = ok ? __ldcg(x + kAttnHD) : -INFINITY;
+        lv[u] = ok ? __ldcg(x + kAttnHD + 1) : 0.f;
+        ov[u] = ok ? __ldcg(reinterpret_cast<const float4*>(x + 4 * lane)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      float bm = M;
+#pragma unroll
+      for (int u = 0; u < kB; ++u) bm = fmaxf(bm, mv[u]);
+      const float corr = M == -INFINITY ? 0.f : ex2(M - bm);
+      den *= corr; num.x *= corr; num.y *= corr; num.z *= corr; num.w *= corr;
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const float w = mv[u] == -INFINITY ? 0.f : ex2(mv[u] - bm);
+        den = fmaf(w, lv[u], den);
+        num.x = fmaf(w, ov[u].x, num.x); num.y = fmaf(w, ov[u].y, num.y);
+        num.z = fmaf(w, ov[u].z, num.z); num.w = fmaf(w, ov[u].w, num.w);
+      }
+      M = bm;
+    }
+    const float inv = 1.f / den;
+    uint2 o2;
+    o2.x = pack_bf16(num.x * inv, num.y * inv);
+    o2.y = pack_bf16(num.z * inv, num.w * inv);
+    *reinterpret_cast<uint2*>(out + size_t(b) * p.q_heads * kAttnHD + (p.kv_head * G + h) * kAttnHD + 4 * lane) = o2;
+  }
+}
+
+// One split of row b is done (its partial written, or it has no tokens):
+// count it; the warp completing the row's n_splits arrivals merges.
+__device__ __forceinline__ void attn_split_arrive(const KArgs& a, const mk_attn_params& p, int b, int pos,
+                                                  int lane) {
+  __threadfence();
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) {
+    const uint32_t old = atom_acq_rel_add(&a.sub_ctr[p.red_ctr0 + b], 1u);
+    last = (old + 1 == uint32_t(p.n_splits) * a.epoch) ? 1 : 0;
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  __threadfence();
+  attn_merge_row(p, b, pos / kAttnSplit + 1, lane);
+}
+
 // Barrier-free variant (one warp per item, wpi = 1): warp w takes the unit's
 // items w, w + 8, ...; each warp waits only for its own item's K/V slots
 // (tag-checked: it may run more than a ring lap ahead), releases them with
@@ -2152,10 +2215,14 @@ __device__ void attn_mma_free(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
     const int b = it / p.n_splits, sp = it % p.n_splits;
     if (b != last_b) { pos = p.positions[b]; last_b = b; }
     const int t0 = sp * kAttnSplit;
-    if (t0 > pos) continue;
+    const bool mine = ((it - ib) & (kConsWarps - 1)) == warp;
+    if (t0 > pos) {                        // no tokens: only the fused-merge arrival
+      if (mine && p.fuse_reduce) attn_split_arrive(a, p, b, pos, lane);
+      continue;
+    }
     const uint32_t kpos = base + 2 * act;
     ++act;
-    if (((it - ib) & (kConsWarps - 1)) != warp) continue;
+    if (!mine) continue;
     uint64_t ph0 = trace ? globaltimer() : 0, ph1 = ph0, ph2 = ph0;
     float m_run = -INFINITY, l_run = 0.f;
     float o[16][4];
@@ -2176,6 +2243,7 @@ __device__ void attn_mma_free(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
         *reinterpret_cast<float2*>(dst + 8 * u + 2 * c) = make_float2(o[u][0], o[u][1]);
       if (c == 0) { dst[kAttnHD] = m_run; dst[kAttnHD + 1] = l_run; }
     }
+    if (p.fuse_reduce) attn_split_arrive(a, p, b, pos, lane);
     if (trace) {
       const uint64_t ph3 = globaltimer();
       phase_rec(a, 2, it, ph0, ph1);
@@ -2213,6 +2281,7 @@ __device__ void run_attn_partial(const KArgs& a, Smem& s, uint8_t* ring, Ring& r
 // up to 16 splits cost one L2 round trip; no barrier.
 __device__ void run_attn_reduce(const KArgs& a, Smem& s, const mk_task& t, int ib, int ie, int ct) {
   const mk_attn_params& p = *P<mk_attn_params>(a, t);
+  if (p.fuse_reduce) return;             // merged by the last split (attn_split_arrive)
   const int HD = p.head_dim, G = p.group;
   const int stride = G * (HD + 4);          // floats per split
   uint16_t* out = reinterpret_cast<uint16_t*>(p.out);

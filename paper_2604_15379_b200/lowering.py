@@ -85,6 +85,8 @@ class LoweringOptions:
                                    # on that task's own predecessor event
     attn_mma: bool = os.environ.get("MK_ATTN_MMA", "1") != "0"
                                    # tensor-core split-KV attention (head_dim 128)
+    fuse_attn_reduce: bool = False # last split of a row merges (ATTN_REDUCE no-op);
+                                   # measured slower (one warp merges serially)
     ksplit: bool = True            # die tasks: K-split slot ranges per worker
                                    # instead of whole tiles
 
@@ -250,9 +252,14 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         p.M, p.d, p.eps = B, d, spec.eps
         return blob.add(p)
 
-    def attn_params(layer, h, out=None):
+    def attn_params(layer, h, out=None, fuse=False, reduce_noop=False):
         lb = bufs.layers[layer]
         p = L.AttnParams()
+        p.fuse_reduce = 1 if reduce_noop else 0
+        if fuse and fused_reduce:
+            p.fuse_reduce = 1
+            p.red_ctr0 = n_sub[0]
+            n_sub[0] += B
         p.qkv = _ptr(lb["qkv_out"])
         p.q_gamma = _ptr(bufs.w_layers[layer]["q_norm"])
         p.k_gamma = _ptr(bufs.w_layers[layer]["k_norm"])
@@ -268,8 +275,7 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         p.eps, p.scale = spec.eps, hd ** -0.5
         # one item per unit (small batch): two warps share each (item, head)
         # and write two partial pieces; otherwise one warp per (item, head)
-        if opts.attn_mma and hd == 128 and bufs.split == 64 and spec.group <= 4 \
-                and B >= ATTN_MMA_MIN_BATCH:
+        if attn_mma:
             p.mma = 1
             # tensor-core path (csrc attn_mma_pass): warps per item so that
             # every consumer warp has work -- 8 / wpi items per pass, whose
@@ -286,6 +292,11 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         return None
 
     gu_fused = g.mode == "chiplet"
+    attn_mma = (opts.attn_mma and hd == 128 and bufs.split == 64 and spec.group <= 4
+                and B >= ATTN_MMA_MIN_BATCH)
+    # barrier-free tensor-core attention merges the splits itself
+    fused_reduce = (attn_mma and opts.fuse_attn_reduce
+                    and int(os.environ.get("MK_ATTN_WPI", "1")) == 1)
     ksplit = opts.ksplit and per_die and bufs.kpart is not None
     fuse = opts.fuse_norm and all(
         stages(B, d, tl) and not is_umma_tile(tl, f)
@@ -375,15 +386,20 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                          po, layer)
         elif op is OpKind.ATTN_PARTIAL:
             h = int(t.id.rsplit(".t", 1)[1])
-            po = attn_params(layer, h)
+            po = attn_params(layer, h, out=lb["attn_out"], fuse=True)
             add_task(t.id, gi, L.OP_ATTN_PARTIAL, level, None, wait,
                      t.signal_event, po, layer, n_items=B * bufs.n_splits,
                      n_units=u_attn)
         elif op is OpKind.ATTN_REDUCE:
             h = int(t.id.rsplit(".t", 1)[1])
-            po = attn_params(layer, h, out=lb["attn_out"])
+            po = attn_params(layer, h, out=lb["attn_out"], reduce_noop=fused_reduce)
+            if fused_reduce:
+                # merged inside ATTN_PARTIAL: the task stays in the graph as a
+                # no-op (one unit), its consumers wait on the partial stage's event
+                bypass[t.signal_event] = wait
             add_task(t.id, gi, L.OP_ATTN_REDUCE, level, None, wait,
-                     t.signal_event, po, layer, n_items=B, n_units=u_attn)
+                     t.signal_event, po, layer, n_items=B,
+                     n_units=1 if fused_reduce else u_attn)
         elif op is OpKind.SILU:
             row0, rows, col0, cols = silu_meta[t.id]
             p = L.SiluParams()

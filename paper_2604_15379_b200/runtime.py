@@ -204,7 +204,7 @@ class Megakernel:
                  sched: str = "per_die", topo: L.Topology | None = None,
                  fanout: bool = True, lm_tile=None, device: int = 0,
                  keep_logits: bool = True, watchdog_s: float = 10.0,
-                 ksplit: bool = True):
+                 ksplit: bool = True, fuse_attn_reduce: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("Megakernel needs a CUDA device (no CPU fallback)")
         self.lib = L.load()
@@ -227,7 +227,8 @@ class Megakernel:
         opts = LoweringOptions(
             sched_mode=L.SCHED_PER_DIE if per_die else L.SCHED_FLAT,
             traversal=traversal, distribution=distribution, workers=workers,
-            n_dies=n_dies, fanout=fanout, lm_tile=lm_tile)
+            n_dies=n_dies, fanout=fanout, lm_tile=lm_tile,
+            fuse_attn_reduce=fuse_attn_reduce)
         v_pad = (-(-self.spec.vocab // 256) * 256) if is_umma_tile(lm_tile, False) \
             else self.spec.vocab
         amax_slots = (n_dies * workers) if per_die else v_pad // lm_tile[1]

@@ -396,3 +396,30 @@ def test_tcgen05_decode_matches_oracle(topo, machine, mode, sched, B, dist, t_m,
     worst, ties = _decode_vs_oracle(mk, w, B, steps=6, t_max=48)
     mk.close()
     assert worst < RTOL
+
+
+def test_fused_attention_reduce_matches_oracle(topo, machine):
+    """Tensor-core attention with the split merge folded into ATTN_PARTIAL
+    (last-arriving split of a row merges; ATTN_REDUCE runs as a no-op and its
+    consumers wait on the partial stage's event)."""
+    import ctypes
+    from paper_2604_15379_b200 import _lib as L
+    from paper_2604_15379_b200.runtime import Megakernel
+    from paper_2604_15379_b200.weights import Qwen3Weights
+    B = 16
+    g, spec = _mini(machine, "chiplet", B)
+    w = Qwen3Weights.random(spec, seed=34)
+    mk = Megakernel(g, w, t_max=160, topo=topo, fuse_attn_reduce=True, watchdog_s=5.0)
+    low = mk.lowered
+    fused = 0
+    for i in range(len(low.tasks)):
+        t = low.tasks[i]
+        if t.op == L.OP_ATTN_PARTIAL:
+            p = L.AttnParams.from_buffer_copy(
+                low.params[t.param_off:t.param_off + ctypes.sizeof(L.AttnParams)])
+            fused += p.fuse_reduce
+    assert fused > 0
+    worst, _ = _decode_vs_oracle(mk, w, B, steps=80, t_max=160)
+    mk.close()
+    assert worst < RTOL
+
