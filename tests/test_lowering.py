@@ -116,3 +116,42 @@ def test_gemm_params_die_slabs():
         assert p.N == n_loc and p.xcd == gt.xcd_binding
         width = n_loc // 2 if p.epilogue == L.EPI_SILU else n_loc
         assert p.y_col0 == gt.xcd_binding * width
+
+
+def _owner(s, S, W):
+    """Inverse of the K-split range starts w*S/W (csrc range_owner)."""
+    return ((s + 1) * W + S - 1) // S - 1
+
+
+def test_ksplit_ranges_cover_every_slot_once_and_pieces_are_consistent():
+    """Host restatement of the device K-split partition (csrc RangeIter /
+    tile_pieces): worker ranges tile the slot sequence exactly once, the
+    owner formula inverts the range starts, and the pieces of every cut tile
+    are the non-empty ranges between the owners of its first and last slot
+    (also when there are more workers than slots)."""
+    for tiles, chunks, W in [(24, 64, 71), (16, 192, 71), (96, 64, 69), (2, 1, 71),
+                             (32, 2, 71), (594, 64, 74), (5, 3, 7)]:
+        S = tiles * chunks
+        starts = [S * w // W for w in range(W + 1)]
+        seen = [0] * S
+        for w in range(W):
+            for s in range(starts[w], starts[w + 1]):
+                seen[s] += 1
+                assert _owner(s, S, W) == w
+        assert seen == [1] * S
+        for t in range(tiles):
+            a, b = t * chunks, t * chunks + chunks - 1
+            fw, lw = _owner(a, S, W), _owner(b, S, W)
+            pieces = [w for w in range(fw, lw + 1) if starts[w] != starts[w + 1]]
+            covering = sorted({_owner(s, S, W) for s in range(a, b + 1)})
+            assert pieces == covering
+
+
+def test_ksplit_pays_only_for_unbalanced_whole_tile_ownership():
+    from paper_2604_15379_b200.lowering import gemv_fast_shape, ksplit_pays
+    assert not ksplit_pays(384, 71)      # B=1 qkv GEMV tiles: 6 rounds, 90% balance
+    assert ksplit_pays(16, 71)           # tcgen05 o_proj / down: 16 tiles, 71 workers
+    assert ksplit_pays(96, 71)           # tcgen05 gate_up: 2 rounds, 68% balance
+    assert not ksplit_pays(142, 71)      # exactly two rounds
+    assert gemv_fast_shape(1, 8, 1024) and gemv_fast_shape(8, 32, 256)
+    assert not gemv_fast_shape(16, 32, 256)
