@@ -423,3 +423,19 @@ def test_fused_attention_reduce_matches_oracle(topo, machine):
     mk.close()
     assert worst < RTOL
 
+
+
+@pytest.mark.parametrize("wpi", ["2", "4"])
+def test_pass_synchronous_attention_matches_oracle(topo, machine, wpi, monkeypatch):
+    """The pass-synchronous tensor-core attention variant (wpi warps per item,
+    cross-warp merge through shared memory), selected by MK_ATTN_WPI."""
+    from paper_2604_15379_b200.runtime import Megakernel
+    from paper_2604_15379_b200.weights import Qwen3Weights
+    monkeypatch.setenv("MK_ATTN_WPI", wpi)
+    B = 16
+    g, spec = _mini(machine, "chiplet", B)
+    w = Qwen3Weights.random(spec, seed=35)
+    mk = Megakernel(g, w, t_max=160, topo=topo, watchdog_s=5.0)
+    worst, _ = _decode_vs_oracle(mk, w, B, steps=70, t_max=160)
+    mk.close()
+    assert worst < RTOL
