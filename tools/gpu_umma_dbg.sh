@@ -1,3 +1,4 @@
+timeout 600 python -m pytest tests -m gpu -x -q -k "tcgen05 or smoke or attention" 2>&1 | tail -2
 python - <<'PY'
 import sys, os, json
 sys.path.insert(0, "tools")
