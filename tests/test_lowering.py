@@ -155,3 +155,53 @@ def test_ksplit_pays_only_for_unbalanced_whole_tile_ownership():
     assert not ksplit_pays(142, 71)      # exactly two rounds
     assert gemv_fast_shape(1, 8, 1024) and gemv_fast_shape(8, 32, 256)
     assert not gemv_fast_shape(16, 32, 256)
+
+
+def _lower_mini(B, **kw):
+    """Qwen3-shaped mini model (head_dim 128): the tensor-core attention path."""
+    from paper_2604_15379_b200.machine import ModelConfig
+    m = ModelConfig(hidden_dim=512, ffn_dim=1024, num_layers=2, q_heads=4, kv_heads=2,
+                    dtype_bytes=2)
+    mach = preset("b200")
+    g = build_decoder_layer(m, mach, "chiplet", B, tile_overrides=device_tiles(m, mach, "chiplet", B),
+                            layers=2)
+    spec = Qwen3Spec(512, 1024, 2, 4, 2, 128, 1024)
+    w = Qwen3Weights.random(spec, seed=2)
+    lm = _default_lm_tile(spec, B)
+    st = build_state(g, w, 128, lm, 2 * W, device="cpu")
+    opts = LoweringOptions(sched_mode=L.SCHED_PER_DIE, workers=W, n_dies=2, lm_tile=lm, **kw)
+    return g, lower(g, spec, st, opts)
+
+
+def _params(low, t, cls):
+    import ctypes
+    return cls.from_buffer_copy(low.params[t.param_off:t.param_off + ctypes.sizeof(cls)])
+
+
+@pytest.mark.parametrize("fuse", [False, True])
+def test_tensor_core_attention_lowering(fuse):
+    """head_dim 128: ATTN_PARTIAL on the tensor-core path (one warp per item);
+    with the fused split merge every row gets an arrival counter, ATTN_REDUCE
+    becomes a one-unit no-op and its consumers wait on the partial stage."""
+    g, low = _lower_mini(16, fuse_attn_reduce=fuse)
+    tasks = [low.tasks[i] for i in range(len(low.tasks))]
+    names = low.task_names
+    ctrs = []
+    for t in tasks:
+        if t.op == L.OP_ATTN_PARTIAL:
+            p = _params(low, t, L.AttnParams)
+            assert p.mma == 1 and p.sub_splits == 1 and p.t_max % 64 == 0
+            assert p.fuse_reduce == (1 if fuse else 0)
+            if fuse:
+                ctrs.append(p.red_ctr0)
+        if t.op == L.OP_ATTN_REDUCE:
+            assert _params(low, t, L.AttnParams).fuse_reduce == (1 if fuse else 0)
+            assert (t.n_units == 1) == fuse
+    if fuse:   # disjoint per-row counters in the sub-counter space
+        assert len(set(ctrs)) == len(ctrs) and max(ctrs) + 16 <= low.n_sub
+    ev = {n: i for i, n in enumerate(low.event_names)}
+    o_proj = [t for t, n in zip(tasks, names) if ".o_proj." in n]
+    want = "attn_partial" if fuse else "attn_reduce"
+    for t in o_proj:
+        assert low.event_names[t.wait0].endswith(want), low.event_names[t.wait0]
+    assert ev  # events lowered
