@@ -74,7 +74,7 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
         "sm__warps_active.avg.pct_of_peak_sustained_active"]
 traffic = {}
-for tag in ("b1", "b64"):
+for tag in ("b1", "b8", "b16", "b64"):
     path = os.path.join(SRC, f"ncu_{tag}_raw.csv")
     if not os.path.exists(path):
         continue
