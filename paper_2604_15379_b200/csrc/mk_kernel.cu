@@ -175,12 +175,28 @@ __host__ __device__ __forceinline__ bool attn_mma_path(const mk_attn_params& p) 
 
 constexpr size_t kSmemBytes = kRingOffset + size_t(kSlots) * kSlotBytes;
 
+// Build split (see __graft_entry__.build): the device code below is compiled
+// once per kernel instance (-DMK_INSTANCE=F, explicit instantiation at the
+// end of the file), the host ABI once (-DMK_HOST_TU) against a declaration.
+#ifndef MK_HOST_TU
+namespace {   // device helpers: internal linkage (compiled into every instance TU)
+
 __device__ __forceinline__ bool aborted(const KArgs& a) {
   return *reinterpret_cast<volatile int*>(a.err) != 0;
 }
 
-__device__ __noinline__ void raise_deadlock(const KArgs& a, int info) {
-  if (atomicCAS(a.err, 0, MK_ERR_DEADLOCK) == 0) *a.err_info = info;
+__device__ __noinline__ void raise_error(const KArgs& a, int code, int info) {
+  if (atomicCAS(a.err, 0, code) == 0) *a.err_info = info;
+}
+__device__ __forceinline__ void raise_deadlock(const KArgs& a, int info) {
+  raise_error(a, MK_ERR_DEADLOCK, info);
+}
+// A decode position outside the allocated KV rows: reported as a config
+// error (info = -100 - row) instead of indexing past the cache / RoPE table.
+__device__ __forceinline__ bool pos_ok(const KArgs& a, int pos, int t_max, int row) {
+  if (pos >= 0 && pos < t_max) return true;
+  raise_error(a, MK_ERR_CONFIG, -100 - row);
+  return false;
 }
 
 // Spin helper: returns false if the watchdog fired / the launch aborted.
@@ -1721,6 +1737,7 @@ __device__ void attn_pass(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   const bool active = item >= 0 && t0 <= pos;
   const int b = active ? item / p.n_splits : 0;
   const int sp = active ? item % p.n_splits : 0;
+  if (active && !pos_ok(a, pos, p.t_max, b)) { pos = p.t_max - 1; has_new = false; }
 
   float q8[8];
   const uint16_t* qkv = reinterpret_cast<const uint16_t*>(p.qkv) + size_t(b) * p.ldqkv;
@@ -2067,6 +2084,7 @@ __device__ void attn_mma_pass(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   const bool active = my_slot >= 0;
   const int b = active ? item / p.n_splits : 0;
   const int sp = active ? item % p.n_splits : 0;
+  if (active && !pos_ok(a, pos, p.t_max, b)) pos = p.t_max - 1;
   const int nvalid = active ? min(kAttnSplit, pos + 1 - t0) : 0;   // incl. the new token
   const int tok0 = sw * tpw;                                         // this warp's tokens
   const bool trace = a.log != nullptr && ct == 0;
@@ -2213,7 +2231,10 @@ __device__ void attn_mma_free(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   const bool trace = a.log != nullptr && lane == 0 && warp == 0;
   for (int it = ib; it < ie; ++it) {
     const int b = it / p.n_splits, sp = it % p.n_splits;
-    if (b != last_b) { pos = p.positions[b]; last_b = b; }
+    if (b != last_b) {
+      pos = p.positions[b]; last_b = b;
+      if (!pos_ok(a, pos, p.t_max, b)) pos = p.t_max - 1;   // garbage, but in bounds
+    }
     const int t0 = sp * kAttnSplit;
     const bool mine = ((it - ib) & (kConsWarps - 1)) == warp;
     if (t0 > pos) {                        // no tokens: only the fused-merge arrival
@@ -2287,8 +2308,7 @@ __device__ void run_attn_reduce(const KArgs& a, Smem& s, const mk_task& t, int i
   uint16_t* out = reinterpret_cast<uint16_t*>(p.out);
   constexpr int kBatch = 20;
   for (int b = ib; b < ie; ++b) {
-    const int pos = p.positions[b];
-    const int nv = pos / p.split + 1;
+    const int nv = min(p.positions[b] / p.split + 1, p.n_splits);
     const float* base = p.partial + (size_t(b) * p.kv_heads + p.kv_head) * p.n_splits * stride;
     for (int e = ct; e < G * HD / 4; e += kCons) {   // 4 dims per thread
       const int hh = (e * 4) / HD, d = (e * 4) % HD;
@@ -2676,6 +2696,8 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
   }
 }
 
+}  // namespace
+
 template <int F>
 __global__ void __launch_bounds__(kThreads, 1) megakernel(const __grid_constant__ KArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -2701,6 +2723,10 @@ __global__ void __launch_bounds__(kThreads, 1) megakernel(const __grid_constant_
   __syncthreads();
   const int g = role[0], rank = role[1];
   if (g >= a.n_sched) return;
+  if (rank < 0 || rank >= a.group_size[g]) {   // role counters out of step with the epoch
+    if (threadIdx.x == 0) raise_error(a, MK_ERR_CONFIG, -200);
+    return;
+  }
   if (rank == 0) {
     if (threadIdx.x < 32) scheduler(a, *reinterpret_cast<SchedSmem*>(ring), g);
     return;
@@ -2744,6 +2770,13 @@ __global__ void __launch_bounds__(kThreads, 1) megakernel(const __grid_constant_
   }
 }
 
+#else
+template <int F>
+__global__ void __launch_bounds__(kThreads, 1) megakernel(const __grid_constant__ KArgs a);
+#endif  // MK_HOST_TU
+
+#ifdef MK_HOST_TU   // the die probe lives with the host ABI
+
 // ---------------------------------------------------------------------------
 // Die probe: per-SM L2 hit latency to lines spread over the address space.
 // ---------------------------------------------------------------------------
@@ -2779,8 +2812,14 @@ __global__ void __launch_bounds__(32, 1) probe_kernel(const uint32_t* buf, int n
   }
 }
 
+#endif  // MK_HOST_TU
 }  // namespace mk
 
+#ifdef MK_INSTANCE
+namespace mk {
+template __global__ void __launch_bounds__(kThreads, 1) megakernel<MK_INSTANCE>(const __grid_constant__ KArgs a);
+}  // namespace mk
+#else  // host ABI
 // ===========================================================================
 // Host side: C ABI
 // ===========================================================================
@@ -3237,7 +3276,6 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
 int mk_step(mk_handle* h, void* stream) {
   if (!h) return fail(MK_ERR_CONFIG, "null handle");
   CK(cudaSetDevice(h->device));
-  h->epoch += 1;
   KArgs a;
   a.tasks = h->d_tasks; a.units = h->d_units; a.sched_begin = h->d_sched_begin;
   a.params = h->d_params; a.ev_ctr = h->d_ev_ctr; a.ev_req = h->d_ev_req;
@@ -3250,7 +3288,7 @@ int mk_step(mk_handle* h, void* stream) {
   a.err = h->d_err; a.err_info = h->d_err + 1;
   a.watchdog_ns = (unsigned long long)(h->watchdog_s * 1e9);
   a.n_events = h->n_events; a.n_sched = h->n_sched; a.sched_mode = h->sched_mode; a.W = h->W;
-  a.epoch = h->epoch;
+  a.epoch = h->epoch + 1;   // committed below, only if the launch was accepted
   a.debug = h->debug;
   a.use_umma = h->use_umma;
   a.tmaps = h->d_tmaps;
@@ -3260,6 +3298,7 @@ int mk_step(mk_handle* h, void* stream) {
   void* args[] = {&a};
   CK(cudaLaunchCooperativeKernel(h->kernel, dim3(h->num_sms), dim3(kThreads), args,
                                  kSmemBytes, static_cast<cudaStream_t>(stream)));
+  h->epoch = a.epoch;
   return MK_OK;
 }
 
@@ -3271,6 +3310,11 @@ int mk_sync(mk_handle* h) {
   if (h->h_err[0] != 0) {
     const int code = h->h_err[0], info = h->h_err[1];
     reset_state(h);
+    if (code == MK_ERR_CONFIG && info <= -100 && info > -200)
+      return fail(code, "decode position of row " + std::to_string(-100 - info) +
+                            " is outside the KV cache (t_max): step aborted");
+    if (code == MK_ERR_CONFIG)
+      return fail(code, "device role assignment out of step (site " + std::to_string(info) + ")");
     return fail(code, "device watchdog: no progress (event/site " + std::to_string(info) + ")");
   }
   return MK_OK;
@@ -3379,3 +3423,5 @@ int mk_destroy(mk_handle* h) {
 }
 
 }  // extern "C"
+
+#endif  // MK_INSTANCE

@@ -109,6 +109,7 @@ class Lowered:
     sched_mode: int
     workers: int
     amax_slots: int
+    kv_swizzled: bool = False      # KV rows chunk-swizzled (tensor-core attention)
     keep: list = field(default_factory=list)   # ctypes arrays kept alive
 
     def desc(self) -> L.GraphDesc:
@@ -474,7 +475,7 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
     r_arr = (C.c_int32 * len(required))(*required)
     return Lowered(t_arr, u_arr, b_arr, r_arr, bytes(blob.data), event_names,
                    names, gidx, n_sub[0], n_sched, opts.sched_mode,
-                   opts.workers, amax_slots)
+                   opts.workers, amax_slots, kv_swizzled=attn_mma)
 
 
 def _silu_meta(g: TaskGraph, B: int, F: int):

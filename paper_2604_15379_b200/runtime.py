@@ -242,6 +242,11 @@ class Megakernel:
         opts.ksplit = ksplit
         self.lowered = lower(g, self.spec, self.state, opts)
         run_topo = topo if per_die else flat_topology(topo.num_sms)
+        # KV cache row layout the lowered attention reads and appends: the
+        # tensor-core path stores every 16-byte chunk of a row XOR-swizzled by
+        # (token & 7) (csrc kv_swz); the CUDA-core path stores rows linear.
+        self.kv_swizzled = self.lowered.kv_swizzled
+        self._pos = torch.zeros(g.batch, dtype=torch.int64)   # host copy of positions
         self._desc = self.lowered.desc()
         h = C.c_void_p()
         L.check(self.lib.mk_create(device, C.byref(self._desc), C.byref(run_topo),
@@ -256,7 +261,57 @@ class Megakernel:
         self.state.tokens.copy_(torch.as_tensor(tokens, dtype=torch.int32))
 
     def set_positions(self, positions):
-        self.state.positions.copy_(torch.as_tensor(positions, dtype=torch.int32))
+        pos = torch.as_tensor(positions, dtype=torch.int64).reshape(-1).cpu()
+        if pos.numel() != self.graph.batch:
+            raise ValueError(f"need {self.graph.batch} positions, got {pos.numel()}")
+        if int(pos.min()) < 0 or int(pos.max()) >= self.state.t_max:
+            raise ValueError(f"positions must lie in [0, t_max={self.state.t_max})")
+        self._pos = pos.clone()
+        self.state.positions.copy_(pos.to(torch.int32))
+
+    def positions(self) -> torch.Tensor:
+        """Host copy of the decode position of every row (the next token's index)."""
+        return self._pos.clone()
+
+    # ---- KV cache (canonical layout [B][kv_head][token][head_dim] bf16) ---
+    def _kv_view(self, buf: torch.Tensor) -> torch.Tensor:
+        """[B, kvh, T, hd] -> [B, kvh, T, hd/8, 8] chunk view."""
+        B, H, T, hd = buf.shape
+        return buf.view(B, H, T, hd // 8, 8)
+
+    def _swizzle_index(self, n: int, device):
+        t = torch.arange(n, device=device).view(n, 1)
+        c = torch.arange(self.spec.head_dim // 8, device=device).view(1, -1)
+        return (c ^ (t & 7))                       # physical chunk of logical chunk c
+
+    def write_kv(self, layer: int, k: torch.Tensor, v: torch.Tensor, n_tokens: int):
+        """Write tokens [0, n_tokens) of canonical K/V ([B, kv_heads, >=n, hd],
+        any dtype) into the device cache in the layout the lowered graph reads
+        (INTEGRATION.md section 4)."""
+        if n_tokens > self.state.t_max:
+            raise ValueError(f"{n_tokens} tokens do not fit t_max={self.state.t_max}")
+        for src, dst in ((k, self.state.k_cache[layer]), (v, self.state.v_cache[layer])):
+            x = src[:, :, :n_tokens].to(dst.device, torch.bfloat16)
+            if self.kv_swizzled:
+                B, H, n, hd = x.shape
+                idx = self._swizzle_index(n, dst.device).view(1, 1, n, hd // 8, 1)
+                out = torch.empty_like(x).view(B, H, n, hd // 8, 8)
+                out.scatter_(3, idx.expand(B, H, n, hd // 8, 8), x.view(B, H, n, hd // 8, 8))
+                x = out.view(B, H, n, hd)
+            dst[:, :, :n_tokens] = x
+
+    def read_kv(self, layer: int, n_tokens: int):
+        """Canonical (un-swizzled) copies of tokens [0, n_tokens) of the cache."""
+        out = []
+        for buf in (self.state.k_cache[layer], self.state.v_cache[layer]):
+            x = buf[:, :, :n_tokens]
+            if self.kv_swizzled:
+                B, H, n, hd = x.shape
+                idx = self._swizzle_index(n, x.device).view(1, 1, n, hd // 8, 1)
+                x = torch.gather(x.reshape(B, H, n, hd // 8, 8), 3,
+                                 idx.expand(B, H, n, hd // 8, 8)).view(B, H, n, hd)
+            out.append(x.clone())
+        return tuple(out)
 
     def fill_kv_random(self, n_tokens: int, seed: int = 99):
         """Perf runs: ``n_tokens`` of synthetic bf16 context per sequence."""
@@ -264,14 +319,21 @@ class Megakernel:
             for j, buf in enumerate((k, v)):
                 n = buf[:, :, :n_tokens].numel()
                 u = hash_uniform(n, seed, 2 * li + j, device=buf.device)
+                # i.i.d. values: the swizzled layout is a permutation of them
                 buf[:, :, :n_tokens] = ((u * 2 - 1) * 1.7).to(torch.bfloat16).view(
                     buf[:, :, :n_tokens].shape)
         self.set_positions([n_tokens] * self.graph.batch)
 
     # ---- execution ---------------------------------------------------------
     def launch(self, stream=None):
+        # every row appends its token at its position: refuse before any row
+        # would index past the cache (the device also flags it, mk_sync)
+        if int(self._pos.max()) >= self.state.t_max:
+            raise L.MkError(L.MK_ERR_CONFIG, f"decode position {int(self._pos.max())} "
+                            f"reached t_max={self.state.t_max}")
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         L.check(self.lib.mk_step(self.h, C.c_void_p(s.cuda_stream)))
+        self._pos += 1                          # the argmax task advances the positions
         self.steps += 1
 
     def sync(self):

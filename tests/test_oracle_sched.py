@@ -56,3 +56,30 @@ def test_per_die_dispatch_order_matches_reference_log(case):
         if action == "dispatch":
             per_die[int(actor.split(".x")[1])].append(tid)
     assert per_die == lists
+
+
+SIMS_W = json.load(open(os.path.join(GOLD, "sim_counters_w.json")))
+
+
+@pytest.mark.parametrize("case", SIMS_W, ids=lambda c: f"W{c['workers']}-{c['model']}")
+def test_counters_match_reference_simulate_any_w(case):
+    """The restatement at every workers-per-die W a probed B200 can give
+    (fixture: ref simulate() at W = 64..77, oracle/gen_sim_w.py)."""
+    from dataclasses import replace
+    from paper_2604_15379_b200.analytics import device_tiles
+    W = case["workers"]
+    base = load_machine(os.path.join(GOLD, "b200_machine.json"))
+    mach = replace(base, cus_per_xcd=W + 1, workers_per_xcd=W)
+    model = model_preset(case["model"])
+    tiles = (fit_tiles(model, mach, "chiplet") if case["tiles"] == "fit"
+             else device_tiles(model, mach, "chiplet", case["batch"]))
+    g = build_decoder_layer(model, mach, "chiplet", case["batch"], tile_overrides=tiles,
+                            layers=case["layers"])
+    exp = expected_counters(g, W)
+    for k in ("dispatches", "fences", "local_atomics", "global_atomics"):
+        assert exp[k] == case[k], k
+    # linear in layers: the 36-layer device check scales the same formula
+    g36 = build_decoder_layer(model, mach, "chiplet", case["batch"], tile_overrides=tiles,
+                              layers=case["layers"] * 3)
+    e36 = expected_counters(g36, W)
+    assert all(e36[k] == 3 * exp[k] for k in exp)
