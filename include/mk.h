@@ -274,6 +274,14 @@ int64_t mk_log_read(mk_handle* h, mk_log_rec* out, int64_t max_records);
 /* Optional tile log: (task, worker, m, n) per GEMM tile (0 = off). */
 int mk_tile_log_enable(mk_handle* h, int64_t capacity);
 int64_t mk_tile_log_read(mk_handle* h, int32_t* out4, int64_t max_records);
+/* Per-unit phase stamps (diagnostics; 0 = off): for every unit a worker
+ * executes, 8 uint64 words {task | item_begin << 32, poll start, dependency
+ * acquired, body start (GEMM operands staged), consumer 0 done, all
+ * consumers done, completion signalled, sequence number}, %globaltimer ns,
+ * laid out [scheduler][worker][units_per_worker][8].  mk_trace_read returns
+ * the total word count. */
+int mk_trace_enable(mk_handle* h, int32_t units_per_worker);
+int64_t mk_trace_read(mk_handle* h, uint64_t* out, int64_t max_words);
 int mk_set_watchdog(mk_handle* h, double seconds);
 /* L2 prefetch run-ahead of each worker (CUDA-core kernel instance), in
  * 16 KiB ring slots beyond the fetch warp (0 = off): weight slots of queued

@@ -111,7 +111,8 @@ class LogRec(C.Structure):
 
 EXPORTS = ("mk_probe", "mk_probe_raw", "mk_create", "mk_step", "mk_sync", "mk_counters_get",
            "mk_counters_reset", "mk_log_enable", "mk_log_read",
-           "mk_tile_log_enable", "mk_tile_log_read", "mk_set_watchdog", "mk_set_debug",
+           "mk_tile_log_enable", "mk_tile_log_read", "mk_trace_enable", "mk_trace_read",
+           "mk_set_watchdog", "mk_set_prefetch", "mk_set_debug",
            "mk_destroy", "mk_last_error", "mk_version")
 
 _lib = None
@@ -141,6 +142,9 @@ def load() -> C.CDLL:
     lib.mk_tile_log_enable.argtypes = [C.c_void_p, C.c_int64]
     lib.mk_tile_log_read.argtypes = [C.c_void_p, C.POINTER(I32), C.c_int64]
     lib.mk_tile_log_read.restype = C.c_int64
+    lib.mk_trace_enable.argtypes = [C.c_void_p, C.c_int32]
+    lib.mk_trace_read.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64]
+    lib.mk_trace_read.restype = C.c_int64
     lib.mk_set_watchdog.argtypes = [C.c_void_p, C.c_double]
     lib.mk_set_debug.argtypes = [C.c_void_p, C.c_int]
     lib.mk_destroy.argtypes = [C.c_void_p]

@@ -118,6 +118,8 @@ struct KArgs {
   int x_stages;            // x ring stages (kXsBytes / x_stage_bytes, <= kXStagesMax)
   int x_stage_bytes;       // 128 * max NT over the graph's tcgen05 tasks
   int pf_slots;            // L2 prefetch run-ahead of the prefetch warp (16 KiB slots)
+  uint64_t* trace;         // per-unit phase stamps [worker][trace_cap][8] (mk_trace_enable)
+  int trace_cap;
 };
 
 struct AttnScratch {
@@ -147,6 +149,7 @@ struct Smem {
   uint64_t tile_done[2], tmem_free[2];
   uint64_t job_full;
   int4 job;                         // {task, worker-in-task, first ring slot, 0}
+  uint64_t tr[8];                   // phase stamps of the current unit (trace)
   uint32_t tmem_base;
   union __align__(1024) {            // 1024: 128B-swizzle atoms of the x ring
     AttnScratch at;
@@ -180,6 +183,10 @@ constexpr size_t kSmemBytes = kRingOffset + size_t(kSlots) * kSlotBytes;
 // end of the file), the host ABI once (-DMK_HOST_TU) against a declaration.
 #ifndef MK_HOST_TU
 namespace {   // device helpers: internal linkage (compiled into every instance TU)
+
+// Phase stamp of the current unit (mk_trace_enable): consumer thread 0 only.
+#define MK_TRACE(a, s, ct, i) \
+  do { if ((a).trace && (ct) == 0) (s).tr[i] = globaltimer(); } while (0)
 
 __device__ __forceinline__ bool aborted(const KArgs& a) {
   return *reinterpret_cast<volatile int*>(a.err) != 0;
@@ -1067,6 +1074,7 @@ __device__ void gemm_task(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
         staged_m = m;
       }
     }
+    if (ct == 0 && a.trace && s.tr[3] == 0) s.tr[3] = globaltimer();
     // fast path for the register-feasible (rows-per-warp, batch) pairs
     const int R = gemm_rows(p);
     bool done = false;
@@ -1155,6 +1163,7 @@ __device__ void gemm_task_ks(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
         staged_m = m;
       }
     }
+    if (ct == 0 && a.trace && s.tr[3] == 0) s.tr[3] = globaltimer();
     // fast path for the register-feasible (rows-per-warp, batch) pairs
     const int R = gemm_rows(p);
     bool done = false;
@@ -1523,6 +1532,7 @@ __device__ void run_gemm_umma(const KArgs& a, Smem& s, Ring& r, const mk_task& t
     s.job = make_int4(tix, w_in_task, int(r.k), 0);
     mbar_arrive(&s.job_full);
   }
+  MK_TRACE(a, s, ct, 3);
   umma_epilogue(a, s, p, w_in_task, ct, tb_k);
   (void)xs_k;
   bar_sync(1, kCons);
@@ -2613,6 +2623,11 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
         const mk_task& t = a.tasks[ent.x];
         const int waits[2] = {t.wait0, t.wait1};
         uint32_t polls = 0;
+        if (a.trace) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) s.tr[i] = 0;
+          s.tr[1] = globaltimer();
+        }
         for (int k = 0; k < 2; ++k) {
           const int e = waits[k];
           if (e < 0) continue;
@@ -2626,6 +2641,7 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
         }
         n_poll += polls;
         if (a.log) t_start = globaltimer();
+        if (a.trace) s.tr[2] = globaltimer();
       }
       s.cur = ent;
       s.abort_flag = aborted(a) ? 1 : 0;
@@ -2651,8 +2667,10 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
       case MK_OP_ARGMAX: run_argmax(a, s, t, ent.y, ent.z, ct); break;
       default: break;
     }
+    MK_TRACE(a, s, ct, 4);
     bar_sync(1, kCons);
     if (ct == 0) {
+      if (a.trace) s.tr[5] = globaltimer();
       ++n_exec;
       if (t.signal >= 0) {
         if (t.level == MK_LEVEL_CHIPLET) {
@@ -2677,6 +2695,14 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
         }
       }
       if (a.log) log_rec(a, 1, ent.x, ent.y, gw, g, t_start, globaltimer());
+      if (a.trace && n_exec <= (unsigned long long)a.trace_cap) {
+        uint64_t* rec = a.trace + (size_t(gw) * a.trace_cap + (n_exec - 1)) * 8;
+        rec[0] = uint64_t(uint32_t(ent.x)) | (uint64_t(uint32_t(ent.y)) << 32);
+#pragma unroll
+        for (int i = 1; i < 6; ++i) rec[i] = s.tr[i];
+        rec[6] = globaltimer();
+        rec[7] = n_exec;
+      }
       mbar_arrive(&s.tq_empty[qi]);
     }
     ++q;
@@ -2855,6 +2881,8 @@ struct mk_handle {
   CUtensorMap* d_tmaps = nullptr; // x tensor map per task (tcgen05 GEMMs)
   int x_stages = 1, x_stage_bytes = 2048;
   int pf_slots = 0;             // L2 prefetch run-ahead per worker (mk_set_prefetch)
+  uint64_t* d_trace = nullptr;  // per-unit phase stamps (mk_trace_enable)
+  int trace_cap = 0;
   // device buffers
   mk_task* d_tasks = nullptr;
   mk_unit* d_units = nullptr;
@@ -3295,6 +3323,8 @@ int mk_step(mk_handle* h, void* stream) {
   a.x_stages = h->x_stages;
   a.x_stage_bytes = h->x_stage_bytes;
   a.pf_slots = h->pf_slots;
+  a.trace = h->trace_cap ? h->d_trace : nullptr;
+  a.trace_cap = h->trace_cap;
   void* args[] = {&a};
   CK(cudaLaunchCooperativeKernel(h->kernel, dim3(h->num_sms), dim3(kThreads), args,
                                  kSmemBytes, static_cast<cudaStream_t>(stream)));
@@ -3390,6 +3420,30 @@ int64_t mk_tile_log_read(mk_handle* h, int32_t* out4, int64_t max_records) {
   return (int64_t)n;
 }
 
+int mk_trace_enable(mk_handle* h, int32_t units_per_worker) {
+  if (!h || units_per_worker < 0) return fail(MK_ERR_CONFIG, "bad trace capacity");
+  CK(cudaSetDevice(h->device));
+  if (h->d_trace) { CK(cudaFree(h->d_trace)); h->d_trace = nullptr; }
+  h->trace_cap = 0;
+  if (units_per_worker > 0) {
+    const size_t n = size_t(h->n_sched) * h->W * units_per_worker * 8;
+    CK(cudaMalloc(&h->d_trace, n * sizeof(uint64_t)));
+    CK(cudaMemset(h->d_trace, 0, n * sizeof(uint64_t)));
+    h->trace_cap = units_per_worker;
+  }
+  return MK_OK;
+}
+
+int64_t mk_trace_read(mk_handle* h, uint64_t* out, int64_t max_words) {
+  if (!h || !out) return -fail(MK_ERR_CONFIG, "null argument");
+  if (cudaSetDevice(h->device) != cudaSuccess) return -MK_ERR_CUDA;
+  const int64_t n = int64_t(h->n_sched) * h->W * h->trace_cap * 8;
+  const int64_t m = std::min(n, max_words);
+  if (m > 0 && cudaMemcpy(out, h->d_trace, m * sizeof(uint64_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -MK_ERR_CUDA;
+  return n;
+}
+
 int mk_set_watchdog(mk_handle* h, double seconds) {
   if (!h || !(seconds > 0)) return fail(MK_ERR_CONFIG, "bad watchdog");
   h->watchdog_s = seconds;
@@ -3416,7 +3470,7 @@ int mk_destroy(mk_handle* h) {
   cudaFree(h->d_mailbox); cudaFree(h->d_mb_head); cudaFree(h->d_mb_tail); cudaFree(h->d_die_of_sm);
   cudaFree(h->d_role_ctr); cudaFree(h->d_group_size); cudaFree(h->d_stats); cudaFree(h->d_err);
   cudaFree(h->d_log); cudaFree(h->d_log_cursor); cudaFree(h->d_tile_log); cudaFree(h->d_tile_cursor);
-  cudaFree(h->d_tmaps);
+  cudaFree(h->d_tmaps); cudaFree(h->d_trace);
   if (h->h_err) cudaFreeHost(h->h_err);
   delete h;
   return MK_OK;

