@@ -22,7 +22,7 @@ sys.path.insert(0, str(ROOT))
 from paper_2604_15379_b200.weights import Qwen3Spec, Qwen3Weights  # noqa: E402
 
 
-def hf_model(w: Qwen3Weights):
+def hf_model(w: Qwen3Weights, device="cpu"):
     from transformers import Qwen3Config, Qwen3ForCausalLM
     sp = w.spec
     cfg = Qwen3Config(vocab_size=sp.vocab, hidden_size=sp.hidden,
@@ -33,7 +33,8 @@ def hf_model(w: Qwen3Weights):
                       max_position_embeddings=4096, tie_word_embeddings=False,
                       attention_bias=False, hidden_act="silu")
     cfg._attn_implementation = "eager"
-    m = Qwen3ForCausalLM(cfg).float().eval()
+    with torch.device(device):
+        m = Qwen3ForCausalLM(cfg).float().eval()
     sd = {"model.embed_tokens.weight": w.embed, "model.norm.weight": w.final_norm,
           "lm_head.weight": w.lm_head}
     for i, L in enumerate(w.layers):

@@ -65,6 +65,7 @@ constexpr int kXStagesMax = 16;                 // UMMA activation ring: up to 1
                                                 //   NT rows x 64 bf16 (128B-swizzled), TMA-fed
 constexpr int kTmemCols = 128;                  // 2 accumulator buffers x 64 columns
 constexpr int kTQ = 32;                         // smem unit queue depth
+constexpr int kPBytes = 192;                    // param block bytes cached per queued unit
 constexpr int kMailbox = 64;                    // mailbox depth per worker
 constexpr uint32_t kEnd = 0xFFFFFFu;
 constexpr int kMaxNB = 16;
@@ -151,6 +152,13 @@ struct Smem {
   int4 job;                         // {task, worker-in-task, first ring slot, 0}
   uint64_t tr[8];                   // phase stamps of the current unit (trace)
   uint32_t tmem_base;
+  // Descriptor cache: the mailbox warp copies every queued unit's task
+  // descriptor and parameter block here, so no role reads them from global
+  // memory on the critical path (an acquire poll invalidates L1, and an L2
+  // round trip costs 1-3 us while HBM streams).  pad[0..1] of the cached
+  // task hold ev_req of its wait events.
+  mk_task tcache[kTQ];
+  uint64_t pcache[kTQ][kPBytes / 8];
   union __align__(1024) {            // 1024: 128B-swizzle atoms of the x ring
     AttnScratch at;
     uint16_t xs[kXsBytes / 2];      // GEMM: staged (normalised) activations
@@ -177,6 +185,8 @@ __host__ __device__ __forceinline__ bool attn_mma_path(const mk_attn_params& p) 
 
 
 constexpr size_t kSmemBytes = kRingOffset + size_t(kSlots) * kSlotBytes;
+static_assert(kSmemBytes <= 232448, "megakernel shared memory exceeds the 227 KB per-CTA limit");
+static_assert(kPBytes == 24 * 8, "the mailbox warp copies 24 param words (lanes 8..31)");
 
 // Build split (see __graft_entry__.build): the device code below is compiled
 // once per kernel instance (-DMK_INSTANCE=F, explicit instantiation at the
@@ -267,9 +277,15 @@ __device__ __forceinline__ bool mbar_wait_p(const KArgs& a, uint64_t* bar, uint3
   return ok;
 }
 
+// Parameter block of a task descriptor from the smem cache (t must be one of
+// Smem::tcache: the block sits in the matching pcache entry).
 template <typename T>
 __device__ __forceinline__ const T* P(const KArgs& a, const mk_task& t) {
-  return reinterpret_cast<const T*>(a.params + t.param_off);
+  static_assert(sizeof(T) <= size_t(kPBytes), "param block exceeds the descriptor cache");
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const Smem& s = *reinterpret_cast<const Smem*>(smem_raw);
+  (void)a;
+  return reinterpret_cast<const T*>(s.pcache[&t - s.tcache]);
 }
 
 // ---------------------------------------------------------------------------
@@ -444,7 +460,7 @@ struct SlotIter {
   __device__ __forceinline__ void init(const KArgs& a, const mk_task& task, int ib_, int ie_, int worker_) {
     t = &task; op = task.op; worker = worker_; ib = ib_; ie = ie_; active = true;
     if (op == MK_OP_GEMM) {
-      const mk_gemm_params& p = *reinterpret_cast<const mk_gemm_params*>(a.params + task.param_off);
+      const mk_gemm_params& p = *P<mk_gemm_params>(a, task);
       it.init(p, a.W, task.level == MK_LEVEL_CHIPLET ? worker : 0);
       w = reinterpret_cast<const __nv_bfloat16*>(p.w);
       R = gemm_rows(p); tk = p.T_K; chunks = p.K / p.T_K; c = c_end = 0; cur_n = 0;
@@ -474,7 +490,7 @@ struct SlotIter {
       ++c;
       return true;
     }
-    const mk_attn_params& p = *reinterpret_cast<const mk_attn_params*>(a.params + t->param_off);
+    const mk_attn_params& p = *P<mk_attn_params>(a, *t);
     if (kv == 1) {   // V block of the current item
       src = reinterpret_cast<const __nv_bfloat16*>(p.v_cache) +
             (reinterpret_cast<const __nv_bfloat16*>(src_k) - reinterpret_cast<const __nv_bfloat16*>(p.k_cache));
@@ -1248,7 +1264,7 @@ __device__ void xload_warp(const KArgs& a, Smem& s) {
     ++jq;
     const int4 job = s.job;
     if (job.x < 0) break;
-    const mk_gemm_params& p = *P<mk_gemm_params>(a, a.tasks[job.x]);
+    const mk_gemm_params& p = *P<mk_gemm_params>(a, s.tcache[job.w]);
     const void* tmap = a.tmaps + job.x;
     const uint32_t x_bytes = uint32_t(umma_nt(p)) * 128u;
     // the consumers acquired the job's input event: order those generic
@@ -1298,7 +1314,7 @@ __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
     ++jq;
     const int4 job = s.job;
     if (job.x < 0) break;
-    const mk_gemm_params& p = *P<mk_gemm_params>(a, a.tasks[job.x]);
+    const mk_gemm_params& p = *P<mk_gemm_params>(a, s.tcache[job.w]);
     const uint32_t idesc = umma_idesc_bf16(128, umma_nt(p));
     // the job starts at the consumers' ring cursor (job.z)
     ri = int(uint32_t(job.z) % kSlots);
@@ -1529,7 +1545,7 @@ __device__ void run_gemm_umma(const KArgs& a, Smem& s, Ring& r, const mk_task& t
   }
   bar_sync(1, kCons);
   if (ct == 0) {
-    s.job = make_int4(tix, w_in_task, int(r.k), 0);
+    s.job = make_int4(tix, w_in_task, int(r.k), int(&t - s.tcache));
     mbar_arrive(&s.job_full);
   }
   MK_TRACE(a, s, ct, 3);
@@ -2488,39 +2504,59 @@ __device__ void scheduler(const KArgs& a, SchedSmem& s, int g) {
 //    each slot into the next free shared-memory ring slot.
 // Splitting them keeps the mailbox's L2 round trips off the ring refill path.
 __device__ void mailbox_warp(const KArgs& a, Smem& s, int g, int worker) {
-  if ((threadIdx.x & 31) != 0) return;
+  const int lane = threadIdx.x & 31;
   const int gw = g * a.W + worker;
   uint64_t head = a.mb_head[gw];
   for (uint32_t q = 0;; ++q) {
     const int qi = q % kTQ;
-    const bool room = mbar_wait(a, &s.tq_empty[qi], ((q / kTQ) & 1) ^ 1, -6);
-    uint64_t e = kEnd;
-    if (room) {
-      Spin sp;
-      const uint64_t* slotp = &a.mailbox[size_t(gw) * kMailbox + head % kMailbox];
-      // relaxed polling (ld.acquire would invalidate this SM's L1 on every
-      // iteration, evicting the other roles' stack data) + one fence
-      for (;;) {
-        e = ld_relaxed64(slotp);
-        if ((e >> 24) == head + 1) break;
-        if (!sp.ok(a, -5)) { e = kEnd; break; }
-        __nanosleep(64);
+    uint32_t payload = kEnd;
+    if (lane == 0) {
+      const bool room = mbar_wait(a, &s.tq_empty[qi], ((q / kTQ) & 1) ^ 1, -6);
+      uint64_t e = kEnd;
+      if (room) {
+        Spin sp;
+        const uint64_t* slotp = &a.mailbox[size_t(gw) * kMailbox + head % kMailbox];
+        // relaxed polling (ld.acquire would invalidate this SM's L1 on every
+        // iteration, evicting the other roles' stack data) + one fence
+        for (;;) {
+          e = ld_relaxed64(slotp);
+          if ((e >> 24) == head + 1) break;
+          if (!sp.ok(a, -5)) { e = kEnd; break; }
+          __nanosleep(64);
+        }
+        fence_acq_rel_gpu();
+        if ((e >> 24) == head + 1) {
+          ++head;
+          st_release64(&a.mb_head[gw], head);
+        }
       }
-      fence_acq_rel_gpu();
-      if ((e >> 24) == head + 1) {
-        ++head;
-        st_release64(&a.mb_head[gw], head);
-      }
+      payload = room ? uint32_t(e & 0xFFFFFFu) : kEnd;
     }
-    const uint32_t payload = uint32_t(e & 0xFFFFFFu);
-    if (payload == kEnd || !room) {
-      s.tq[qi] = make_int4(-1, 0, 0, 0);
-      mbar_arrive(&s.tq_full[qi]);
+    payload = __shfl_sync(0xffffffffu, payload, 0);
+    if (payload == kEnd) {
+      if (lane == 0) {
+        s.tq[qi] = make_int4(-1, 0, 0, 0);
+        mbar_arrive(&s.tq_full[qi]);
+      }
       return;
     }
+    // the unit's task descriptor (8 words) and parameter block (kPBytes)
+    // into the descriptor cache, one 8-byte word per lane
     const mk_unit u = a.units[payload];
-    s.tq[qi] = make_int4(u.task, u.item_begin, u.item_end, 0);
-    mbar_arrive(&s.tq_full[qi]);
+    const mk_task* gt = a.tasks + u.task;
+    const uint64_t* src = lane < 8 ? reinterpret_cast<const uint64_t*>(gt) + lane
+                                   : reinterpret_cast<const uint64_t*>(a.params + gt->param_off) + (lane - 8);
+    const uint64_t v = *src;
+    if (lane < 8) reinterpret_cast<uint64_t*>(&s.tcache[qi])[lane] = v;
+    else s.pcache[qi][lane - 8] = v;
+    __syncwarp();
+    if (lane == 0) {
+      mk_task& t = s.tcache[qi];
+      t.pad[0] = t.wait0 >= 0 ? a.ev_req[t.wait0] : 0;
+      t.pad[1] = t.wait1 >= 0 ? a.ev_req[t.wait1] : 0;
+      s.tq[qi] = make_int4(u.task, u.item_begin, u.item_end, 0);
+      mbar_arrive(&s.tq_full[qi]);
+    }
   }
 }
 
@@ -2548,8 +2584,8 @@ __device__ void prefetch_warp(const KArgs& a, Smem& s, int worker) {
     const int4 ent = s.tq[qi];
     if (ent.x < 0) return;
     SlotIter<F> it;
-    it.init(a, a.tasks[ent.x], ent.y, ent.z, worker);
-    const bool gemm = a.tasks[ent.x].op == MK_OP_GEMM;
+    it.init(a, s.tcache[qi], ent.y, ent.z, worker);
+    const bool gemm = s.tcache[qi].op == MK_OP_GEMM;
     const void* src;
     uint32_t bytes;
     while (it.next(a, src, bytes)) {
@@ -2583,7 +2619,7 @@ __device__ void ring_warp(const KArgs& a, Smem& s, uint8_t* ring, int worker) {
     const int4 ent = s.tq[qi];
     if (ent.x < 0) return;
     SlotIter<F> it;
-    it.init(a, a.tasks[ent.x], ent.y, ent.z, worker);
+    it.init(a, s.tcache[qi], ent.y, ent.z, worker);
     const void* src;
     uint32_t bytes;
     while (it.next(a, src, bytes)) {
@@ -2620,7 +2656,7 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
       int4 ent = make_int4(-1, 0, 0, 0);
       if (mbar_wait(a, &s.tq_full[qi], (q / kTQ) & 1, -7)) ent = s.tq[qi];
       if (ent.x >= 0) {
-        const mk_task& t = a.tasks[ent.x];
+        const mk_task& t = s.tcache[qi];
         const int waits[2] = {t.wait0, t.wait1};
         uint32_t polls = 0;
         if (a.trace) {
@@ -2631,7 +2667,7 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
         for (int k = 0; k < 2; ++k) {
           const int e = waits[k];
           if (e < 0) continue;
-          const uint32_t target = uint32_t(a.ev_req[e]) * a.epoch;
+          const uint32_t target = uint32_t(t.pad[k]) * a.epoch;   // cached ev_req[e]
           Spin sp;
           for (;;) {
             ++polls;
@@ -2649,7 +2685,7 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
     bar_sync(1, kCons);
     const int4 ent = s.cur;
     if (ent.x < 0 || s.abort_flag) break;
-    const mk_task& t = a.tasks[ent.x];
+    const mk_task& t = s.tcache[qi];
     switch (t.op) {
       case MK_OP_GEMM:
         if constexpr ((F & kFeatUmma) != 0) {
@@ -3240,7 +3276,7 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
   DA(h->d_tasks, g->n_tasks);
   DA(h->d_units, g->n_units);
   DA(h->d_sched_begin, g->n_schedulers + 1);
-  DA(h->d_params, g->param_bytes);
+  DA(h->d_params, g->param_bytes + kPBytes);   // the cache copy reads kPBytes per block
   DA(h->d_ev_ctr, g->n_events);
   DA(h->d_ev_req, g->n_events);
   DA(h->d_die_ctr, size_t(g->n_events) * g->n_schedulers);
@@ -3261,6 +3297,7 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
   CK(cudaMemcpy(h->d_units, g->units, sizeof(mk_unit) * g->n_units, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(h->d_sched_begin, g->sched_begin, sizeof(int32_t) * (g->n_schedulers + 1),
                 cudaMemcpyHostToDevice));
+  CK(cudaMemset(h->d_params, 0, g->param_bytes + kPBytes));
   if (g->param_bytes)
     CK(cudaMemcpy(h->d_params, g->params, g->param_bytes, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(h->d_ev_req, g->event_required, sizeof(int32_t) * g->n_events, cudaMemcpyHostToDevice));

@@ -45,7 +45,7 @@ def is_umma_tile(tile, fused: bool) -> bool:
     return t_k == 64 and t_n * (2 if fused else 1) == 128
 
 
-KSPLIT_MIN_BALANCE = 0.85
+KSPLIT_MIN_BALANCE = float(os.environ.get("MK_KSPLIT_BALANCE", "0.85"))
 # tensor-core attention from this batch on (barrier-free warps: measured
 # faster than the CUDA-core split path at every batch 1-64)
 ATTN_MMA_MIN_BATCH = int(os.environ.get("MK_ATTN_MMA_MIN_BATCH", "1"))
