@@ -220,6 +220,10 @@ typedef struct mk_graph_desc {
   const mk_unit* units;      /* units grouped per scheduler, topological order */
   const int32_t* sched_begin;/* [n_schedulers+1] offsets into units           */
   const void* params;        /* param blob                                    */
+  const int32_t* positions;  /* device [n_rows]: decode position of every row,
+                                read once per launch (borrowed)               */
+  int32_t n_rows;
+  int32_t pad;
 } mk_graph_desc;
 
 typedef struct mk_counters {

@@ -89,7 +89,8 @@ class GraphDesc(C.Structure):
                 ("n_sub_ctrs", I32), ("n_schedulers", I32), ("sched_mode", I32),
                 ("workers_per_sched", I32), ("param_bytes", I32),
                 ("tasks", P), ("event_required", P), ("units", P),
-                ("sched_begin", P), ("params", P)]
+                ("sched_begin", P), ("params", P), ("positions", P), ("n_rows", I32),
+                ("pad", I32)]
 
 
 class Counters(C.Structure):

@@ -66,6 +66,7 @@ constexpr int kXStagesMax = 16;                 // UMMA activation ring: up to 1
 constexpr int kTmemCols = 128;                  // 2 accumulator buffers x 64 columns
 constexpr int kTQ = 32;                         // smem unit queue depth
 constexpr int kPBytes = 192;                    // param block bytes cached per queued unit
+constexpr int kPosRows = 256;                   // decode positions cached per CTA
 constexpr int kMailbox = 64;                    // mailbox depth per worker
 constexpr uint32_t kEnd = 0xFFFFFFu;
 constexpr int kMaxNB = 16;
@@ -119,6 +120,8 @@ struct KArgs {
   int x_stages;            // x ring stages (kXsBytes / x_stage_bytes, <= kXStagesMax)
   int x_stage_bytes;       // 128 * max NT over the graph's tcgen05 tasks
   int pf_slots;            // L2 prefetch run-ahead of the prefetch warp (16 KiB slots)
+  const int32_t* positions; // decode position per row (read once per launch into smem)
+  int n_rows;
   uint64_t* trace;         // per-unit phase stamps [worker][trace_cap][8] (mk_trace_enable)
   int trace_cap;
 };
@@ -157,7 +160,9 @@ struct Smem {
   // memory on the critical path (an acquire poll invalidates L1, and an L2
   // round trip costs 1-3 us while HBM streams).  pad[0..1] of the cached
   // task hold ev_req of its wait events.
-  mk_task tcache[kTQ];
+  int32_t pos[kPosRows];            // positions[] at launch (advanced only by the last task)
+  int32_t n_pos;                    // rows cached in pos[]
+  alignas(16) mk_task tcache[kTQ];
   uint64_t pcache[kTQ][kPBytes / 8];
   union __align__(1024) {            // 1024: 128B-swizzle atoms of the x ring
     AttnScratch at;
@@ -275,6 +280,14 @@ __device__ __forceinline__ bool mbar_wait_p(const KArgs& a, uint64_t* bar, uint3
   const bool ok = mbar_spin(a, bar, parity, info);
   acc += (unsigned long long)(clock64() - t0);
   return ok;
+}
+
+// Decode position of row b: the launch-time smem copy (positions change only
+// in the step's final ARGMAX task), global memory beyond kPosRows rows.
+__device__ __forceinline__ int row_pos(const int32_t* gpos, int b) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const Smem& s = *reinterpret_cast<const Smem*>(smem_raw);
+  return b < s.n_pos ? s.pos[b] : gpos[b];
 }
 
 // Parameter block of a task descriptor from the smem cache (t must be one of
@@ -500,7 +513,7 @@ struct SlotIter {
     const bool full = attn_mma_path(p);   // tensor-core path: whole 64-token blocks
     for (; item < ie; ++item) {
       const int b = item / p.n_splits, sp = item % p.n_splits;
-      const int pos = p.positions[b];
+      const int pos = row_pos(p.positions, b);
       const int t0 = sp * p.split;
       if (t0 > pos) continue;
       const int nc = full ? p.split : min(p.split, pos - t0);
@@ -1750,7 +1763,7 @@ __device__ void attn_pass(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   bool has_new = false;
   for (int it = i0; it < i1; ++it) {
     const int b = it / p.n_splits, sp = it % p.n_splits;
-    const int ps = p.positions[b];
+    const int ps = row_pos(p.positions, b);
     const int tt0 = sp * p.split;
     const int nci = tt0 > ps ? 0 : min(p.split, ps - tt0);
     if (it - i0 == slot_item) {
@@ -2102,7 +2115,7 @@ __device__ void attn_mma_pass(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   int my_slot = -1, n_slots = 0, item = -1, pos = 0, t0 = 0;
   for (int it = i0; it < i1; ++it) {
     const int b = it / p.n_splits, sp = it % p.n_splits;
-    const int ps = p.positions[b];
+    const int ps = row_pos(p.positions, b);
     const int tt0 = sp * kAttnSplit;
     if (it - i0 == slot_item) { item = it; pos = ps; t0 = tt0; if (tt0 <= ps) my_slot = n_slots; }
     if (tt0 <= ps) n_slots += 2;
@@ -2258,7 +2271,7 @@ __device__ void attn_mma_free(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   for (int it = ib; it < ie; ++it) {
     const int b = it / p.n_splits, sp = it % p.n_splits;
     if (b != last_b) {
-      pos = p.positions[b]; last_b = b;
+      pos = row_pos(p.positions, b); last_b = b;
       if (!pos_ok(a, pos, p.t_max, b)) pos = p.t_max - 1;   // garbage, but in bounds
     }
     const int t0 = sp * kAttnSplit;
@@ -2334,7 +2347,7 @@ __device__ void run_attn_reduce(const KArgs& a, Smem& s, const mk_task& t, int i
   uint16_t* out = reinterpret_cast<uint16_t*>(p.out);
   constexpr int kBatch = 20;
   for (int b = ib; b < ie; ++b) {
-    const int nv = min(p.positions[b] / p.split + 1, p.n_splits);
+    const int nv = min(row_pos(p.positions, b) / p.split + 1, p.n_splits);
     const float* base = p.partial + (size_t(b) * p.kv_heads + p.kv_head) * p.n_splits * stride;
     for (int e = ct; e < G * HD / 4; e += kCons) {   // 4 dims per thread
       const int hh = (e * 4) / HD, d = (e * 4) % HD;
@@ -2782,6 +2795,8 @@ __global__ void __launch_bounds__(kThreads, 1) megakernel(const __grid_constant_
     fence_mbar_init();
     if (blockIdx.x == 0) atomicAdd(&a.stats[S_STEPS], 1ull);
   }
+  for (int i = threadIdx.x; i < a.n_rows && i < kPosRows; i += blockDim.x) s.pos[i] = a.positions[i];
+  if (threadIdx.x == 0) s.n_pos = a.positions ? min(a.n_rows, kPosRows) : 0;
   __syncthreads();
   const int g = role[0], rank = role[1];
   if (g >= a.n_sched) return;
@@ -2918,6 +2933,8 @@ struct mk_handle {
   int x_stages = 1, x_stage_bytes = 2048;
   int pf_slots = 0;             // L2 prefetch run-ahead per worker (mk_set_prefetch)
   uint64_t* d_trace = nullptr;  // per-unit phase stamps (mk_trace_enable)
+  const int32_t* positions = nullptr;  // borrowed: decode position per row
+  int n_rows = 0;
   int trace_cap = 0;
   // device buffers
   mk_task* d_tasks = nullptr;
@@ -3251,6 +3268,8 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
   h->n_tasks = g->n_tasks;
   h->n_units = g->n_units;
   h->n_sub = g->n_sub_ctrs;
+  h->positions = g->positions;
+  h->n_rows = g->positions ? g->n_rows : 0;
   std::vector<int8_t> die_of_sm(MK_MAX_SMS, 0);
   h->group_size.assign(MK_MAX_DIES, 0);
   if (g->sched_mode == MK_SCHED_FLAT) {
@@ -3361,6 +3380,7 @@ int mk_step(mk_handle* h, void* stream) {
   a.x_stage_bytes = h->x_stage_bytes;
   a.pf_slots = h->pf_slots;
   a.trace = h->trace_cap ? h->d_trace : nullptr;
+  a.positions = h->positions; a.n_rows = h->n_rows;
   a.trace_cap = h->trace_cap;
   void* args[] = {&a};
   CK(cudaLaunchCooperativeKernel(h->kernel, dim3(h->num_sms), dim3(kThreads), args,

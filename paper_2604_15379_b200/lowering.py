@@ -110,6 +110,8 @@ class Lowered:
     workers: int
     amax_slots: int
     kv_swizzled: bool = False      # KV rows chunk-swizzled (tensor-core attention)
+    positions: int = 0             # device pointer of the per-row decode positions
+    n_rows: int = 0
     keep: list = field(default_factory=list)   # ctypes arrays kept alive
 
     def desc(self) -> L.GraphDesc:
@@ -129,6 +131,8 @@ class Lowered:
         g.units = C.cast(self.units, C.c_void_p)
         g.sched_begin = C.cast(self.sched_begin, C.c_void_p)
         g.params = C.cast(pbuf, C.c_void_p)
+        g.positions = self.positions
+        g.n_rows = self.n_rows
         return g
 
 
@@ -475,7 +479,8 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
     r_arr = (C.c_int32 * len(required))(*required)
     return Lowered(t_arr, u_arr, b_arr, r_arr, bytes(blob.data), event_names,
                    names, gidx, n_sub[0], n_sched, opts.sched_mode,
-                   opts.workers, amax_slots, kv_swizzled=attn_mma)
+                   opts.workers, amax_slots, kv_swizzled=attn_mma,
+                   positions=_ptr(bufs.positions) or 0, n_rows=B)
 
 
 def _silu_meta(g: TaskGraph, B: int, F: int):
