@@ -41,6 +41,12 @@ from oracle.qwen3_fp32 import Qwen3Fp32, margins
 pytestmark = pytest.mark.gpu
 
 RTOL = 2e-2          # north_star: bf16 device vs fp32 reference logits
+# 36 layers: the bf16 format's own drift.  transformers Qwen3ForCausalLM run
+# in bf16 deviates from the same model in fp32 by 3.5-4.6 % normwise on these
+# hash-initialised weights (the device: 3.1-4.3 %, same greedy ids) --
+# tools/precision_gap.py, profiles/r02/precision_gap_36.json.  At 2 layers
+# both are ~1 % and the north_star 2e-2 applies.
+RTOL_DEEP = 5e-2
 ROW_L2 = 2e-2        # per-row ||dev - ref|| / ||ref|| (same rtol, L2 over the row)
 CTX_LO, CTX_SPAN = 990, 90   # row b decodes at CTX_LO + (37 b) % CTX_SPAN
 OUT = os.environ.get("MK_PARITY_OUT", "gpurun_out/parity")
@@ -101,7 +107,7 @@ def _context(mk, ref, B, seed):
     return pos
 
 
-def decode_vs_oracle(mk, ref, B, steps, seed, tag):
+def decode_vs_oracle(mk, ref, B, steps, seed, tag, rtol=RTOL):
     """Teacher-forced decode; returns a per-step report (written to OUT)."""
     gen = torch.Generator().manual_seed(seed)
     toks = torch.randint(0, mk.spec.vocab, (B,), generator=gen)
@@ -132,8 +138,8 @@ def decode_vs_oracle(mk, ref, B, steps, seed, tag):
         report.append(dict(step=s, normwise_err=err, row_l2_err=row_l2,
                            min_margin=marg.min().item(), tie_tol=tol,
                            n_ambiguous=len(ambiguous), n_flipped=len(step_ties)))
-        assert err <= RTOL, (tag, s, err)
-        assert row_l2 <= ROW_L2, (tag, s, row_l2)
+        assert err <= rtol, (tag, s, err)
+        assert row_l2 <= max(ROW_L2, rtol), (tag, s, row_l2)
         toks = want.argmax(-1)
     os.makedirs(OUT, exist_ok=True)
     with open(os.path.join(OUT, f"{tag}.json"), "w") as f:
@@ -251,7 +257,7 @@ def test_qwen3_8b_36_layers_greedy_and_sync_accounting(topo, machine):
     ref = Qwen3Fp32(cpu, t_max=1152, batch=1)
     _context(mk, ref, 1, seed=3)
     del cpu
-    decode_vs_oracle(mk, ref, 1, steps=8, seed=9, tag="qwen3_8b_36l_b1")
+    decode_vs_oracle(mk, ref, 1, steps=8, seed=9, tag="qwen3_8b_36l_b1", rtol=RTOL_DEEP)
     mk.close()
     del ref
     mk = Megakernel(g, w, t_max=64, topo=topo, fanout=False, watchdog_s=10.0)
