@@ -39,12 +39,21 @@ def rotate_half(x: torch.Tensor) -> torch.Tensor:
 
 
 class Qwen3Fp32:
-    """Sequential decode with an fp32 KV cache, batch rows independent."""
+    """Sequential decode with an fp32 KV cache, batch rows independent.
 
-    def __init__(self, weights, t_max: int, batch: int):
+    ``dtype=torch.bfloat16`` (on any ``device``) instead restates the same
+    model executed the way ``Qwen3ForCausalLM.to(torch.bfloat16)`` executes
+    it: bf16 weights, activations and KV cache, every op rounding its output
+    to bf16, RMSNorm statistics and the softmax in fp32 then cast back
+    (modeling_qwen3.py:50-64, 196-219).  It is not the oracle: the GPU
+    parity test uses it to measure the bf16 format's own drift from fp32 at
+    36 layers, the yardstick the device's deviation is held to."""
+
+    def __init__(self, weights, t_max: int, batch: int, dtype=torch.float32, device="cpu"):
         sp = weights.spec
         self.spec = sp
-        f32 = lambda t: t.detach().to("cpu", torch.float32)  # noqa: E731
+        self.dt = dtype
+        f32 = lambda t: t.detach().to(device, dtype)  # noqa: E731
         self.embed = f32(weights.embed)
         self.final_norm = f32(weights.final_norm)
         self.lm_head = f32(weights.lm_head)
@@ -57,22 +66,25 @@ class Qwen3Fp32:
         pos = torch.arange(t_max, dtype=torch.float32)
         freqs = pos[:, None] * inv[None, :]
         emb = torch.cat((freqs, freqs), dim=-1)
-        self.cos, self.sin = emb.cos(), emb.sin()
-        self.k = [torch.zeros(batch, sp.kv_heads, t_max, hd) for _ in self.layers]
-        self.v = [torch.zeros(batch, sp.kv_heads, t_max, hd) for _ in self.layers]
+        self.cos, self.sin = emb.cos().to(device, dtype), emb.sin().to(device, dtype)
+        self.k = [torch.zeros(batch, sp.kv_heads, t_max, hd, device=device, dtype=dtype)
+                  for _ in self.layers]
+        self.v = [torch.zeros(batch, sp.kv_heads, t_max, hd, device=device, dtype=dtype)
+                  for _ in self.layers]
         self.pos = torch.zeros(batch, dtype=torch.int64)
 
     def load_kv(self, layer: int, k: torch.Tensor, v: torch.Tensor, n: int):
         """Seed the cache with ``n`` tokens (fp32 copies of device bf16 KV)."""
-        self.k[layer][:, :, :n] = k[:, :, :n].float()
-        self.v[layer][:, :, :n] = v[:, :, :n].float()
+        self.k[layer][:, :, :n] = k[:, :, :n].to(self.k[layer])
+        self.v[layer][:, :, :n] = v[:, :, :n].to(self.v[layer])
 
     @torch.no_grad()
     def step(self, tokens: torch.Tensor, layers: int | None = None) -> torch.Tensor:
         """Decode one token per row at ``self.pos``; returns fp32 logits [B, V]."""
         sp = self.spec
         B, hd, G = tokens.shape[0], sp.head_dim, sp.group
-        x = self.embed[tokens.long()]                       # [B, d]
+        rms_norm = self._norm
+        x = self.embed[tokens.long().to(self.embed.device)]  # [B, d]
         n_layers = len(self.layers) if layers is None else layers
         for li in range(n_layers):
             L = self.layers[li]
@@ -82,7 +94,7 @@ class Qwen3Fp32:
             v = (h @ L["v"].T).view(B, sp.kv_heads, hd)
             q = rms_norm(q, L["q_norm"], sp.eps)
             k = rms_norm(k, L["k_norm"], sp.eps)
-            out = torch.empty(B, sp.q_heads, hd)
+            out = torch.empty(B, sp.q_heads, hd, device=x.device, dtype=x.dtype)
             for b in range(B):
                 p = int(self.pos[b])
                 c, s = self.cos[p], self.sin[p]
@@ -95,7 +107,7 @@ class Qwen3Fp32:
                 keys = keys.repeat_interleave(G, dim=0)      # repeat_kv
                 vals = vals.repeat_interleave(G, dim=0)
                 att = (qb[:, None, :] @ keys.transpose(1, 2)) * hd ** -0.5
-                att = torch.softmax(att, dim=-1)
+                att = torch.softmax(att.float(), dim=-1).to(att.dtype)
                 out[b] = (att @ vals)[:, 0, :]
             x = x + out.reshape(B, -1) @ L["o"].T
             h = rms_norm(x, L["post_norm"], sp.eps)
@@ -104,7 +116,14 @@ class Qwen3Fp32:
             x = x + (torch.nn.functional.silu(g) * u) @ L["down"].T
         self.pos += 1
         h = rms_norm(x, self.final_norm, sp.eps)
-        return h @ self.lm_head.T
+        return (h @ self.lm_head.T).float().cpu()
+
+    def _norm(self, x: torch.Tensor, g: torch.Tensor, eps: float) -> torch.Tensor:
+        if self.dt == torch.float32:
+            return rms_norm(x, g, eps)
+        # Qwen3RMSNorm under bf16: fp32 statistics, cast, then gamma in bf16
+        xf = x.float()
+        return g * (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + eps)).to(x.dtype)
 
 
 def greedy(logits: torch.Tensor) -> torch.Tensor:

@@ -58,3 +58,39 @@ def test_pack_gate_up_fused_layout():
     blk = p[1, 1, 0]
     assert torch.equal(blk[0], g[6:8, 0:2])
     assert torch.equal(blk[1], u[6:8, 0:2])
+
+
+@torch.no_grad()
+def test_bf16_restatement_matches_transformers_bf16():
+    """Qwen3Fp32(dtype=bf16) -- the 36-layer GPU test's yardstick for the bf16
+    format's own drift -- restates Qwen3ForCausalLM.to(bfloat16): decoded
+    token by token on the toy model its logits are bit-identical to
+    transformers' bf16 ones while the context is short (3 steps), and its
+    drift from fp32 stays the size of transformers-bf16's afterwards (bf16
+    matmul batching differs once the attention spans more keys)."""
+    pytest.importorskip("transformers")
+    from transformers import DynamicCache
+
+    from oracle.gen_hf_golden import hf_model
+    spec = Qwen3Spec.toy()
+    w = Qwen3Weights.random(spec, seed=7)
+    m = hf_model(w).to(torch.bfloat16)
+    B, T = 2, 8
+    tokens = torch.randint(0, spec.vocab, (B, T), generator=torch.Generator().manual_seed(5))
+    o16 = Qwen3Fp32(w, t_max=T + 4, batch=B, dtype=torch.bfloat16)
+    o32 = Qwen3Fp32(w, t_max=T + 4, batch=B)
+    cache = DynamicCache()
+    gaps16, gaps32 = [], []
+    for t in range(T):
+        out = m(input_ids=tokens[:, t:t + 1], past_key_values=cache, use_cache=True,
+                position_ids=torch.full((B, 1), t, dtype=torch.long))
+        cache = out.past_key_values
+        hf16 = out.logits[:, 0].float()
+        a, b = o16.step(tokens[:, t]), o32.step(tokens[:, t])
+        assert a.dtype == torch.float32
+        if t < 3:
+            assert torch.equal(a, hf16), t
+        scale = b.abs().max().item()
+        gaps16.append((a - b).abs().max().item() / scale)
+        gaps32.append((hf16 - b).abs().max().item() / scale)
+    assert 0.5 * max(gaps32) <= max(gaps16) <= 2 * max(gaps32), (gaps16, gaps32)
