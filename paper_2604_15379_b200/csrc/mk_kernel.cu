@@ -36,6 +36,7 @@
 #include <cuda_runtime.h>
 #include <cooperative_groups.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cmath>
 #include <vector>
@@ -75,6 +76,13 @@ constexpr int kMaxNB = 16;
 // K-split code (smaller code, same register allocation as the plain GEMV).
 constexpr int kFeatUmma = 1;      // tcgen05 GEMM body, MMA warp, TMEM
 constexpr int kFeatKsplit = 2;    // K-split die tasks (partial pieces)
+// Lean instances: only the op bodies a batch-1 GEMV graph (F = Lean|Ksplit)
+// or an all-tcgen05 graph (F = Lean|Umma|Ksplit) executes.  The general
+// instances carry every batch width's unrolled GEMV body (0.1-0.24 M SASS
+// instructions, 1.7-3.9 MB of code); each op switch of a decode step then
+// refetches its code through the instruction caches from L2 while HBM
+// streams.
+constexpr int kFeatLean = 4;
 constexpr int kAmaxRows = 64;
 
 enum StatIdx {
@@ -572,7 +580,7 @@ __device__ __forceinline__ void dot8_acc(const float (&w)[8], const float (&x)[8
 // Stage rows [m0, m0+rows) of x (K wide) into s.u.xs, optionally applying
 // Qwen3RMSNorm (fp32 statistics, cast, gamma) -- the rms task fused into its
 // consumer GEMM.  Bit-identical to run_rmsnorm's output.
-__device__ void stage_x(Smem& s, const mk_gemm_params& p, int m0, int rows, int ct) {
+__device__ void stage_x(Smem& s, const mk_gemm_params& p, int m0, int rows, int ct, bool trace) {
   const uint16_t* x = reinterpret_cast<const uint16_t*>(p.x);
   const int K = p.K;
   const bool norm = p.norm_gamma != nullptr;
@@ -604,6 +612,7 @@ __device__ void stage_x(Smem& s, const mk_gemm_params& p, int m0, int rows, int 
       }
     }
   }
+  if (trace && ct == 0 && s.tr[7] == 0) s.tr[7] = globaltimer();
   if (norm) {
     const int warp = ct >> 5, lane = ct & 31;
 #pragma unroll
@@ -1099,7 +1108,7 @@ __device__ void gemm_task(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
     cur_m = m;
     if constexpr (XS) {
       if (m != staged_m) {
-        stage_x(s, p, m * p.T_M, min(p.T_M, p.M - m * p.T_M), ct);
+        stage_x(s, p, m * p.T_M, min(p.T_M, p.M - m * p.T_M), ct, a.trace != nullptr);
         staged_m = m;
       }
     }
@@ -1188,7 +1197,7 @@ __device__ void gemm_task_ks(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
     cur_m = m;
     if constexpr (XS) {
       if (m != staged_m) {
-        stage_x(s, p, m * p.T_M, min(p.T_M, p.M - m * p.T_M), ct);
+        stage_x(s, p, m * p.T_M, min(p.T_M, p.M - m * p.T_M), ct, a.trace != nullptr);
         staged_m = m;
       }
     }
@@ -1599,6 +1608,18 @@ __device__ void run_gemm(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
       s.amx_idx[e / kAmaxRows][e % kAmaxRows] = 0x7fffffff;
     }
     bar_sync(1, kCons);
+  }
+  if constexpr ((F & kFeatLean) != 0) {
+    if constexpr ((F & kFeatUmma) == 0) {          // batch-1 bodies only
+      if (p.ksplit) {
+        if (p.stage_x) gemm_task_ks<1, true>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles);
+        else gemm_task_ks<1, false>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles);
+      } else if (p.stage_x) gemm_task<1, true>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles);
+      else gemm_task<1, false>(a, s, ring, r, p, w_in_task, gw, tix, ct, tiles);
+    } else if (ct == 0) {
+      raise_error(a, MK_ERR_CONFIG, -300);         // mk_create picked the wrong instance
+    }
+    return;
   }
   const int rows = min(p.T_M, p.M);
 #define MK_GEMM_NB(XSV)                                                              \
@@ -2314,9 +2335,15 @@ __device__ void attn_mma_free(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   r.k = base + 2 * act;
 }
 
+template <int F>
 __device__ void run_attn_partial(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
                                  const mk_task& t, int ib, int ie, int ct) {
   const mk_attn_params& p = *P<mk_attn_params>(a, t);
+  if constexpr ((F & kFeatLean) != 0) {    // lean: the one-warp-per-item tensor-core path
+    if (attn_mma_path(p) && p.sub_splits == 1) attn_mma_free(a, s, ring, r, p, ib, ie, ct);
+    else if (ct == 0) raise_error(a, MK_ERR_CONFIG, -301);
+    return;
+  }
   if (attn_mma_path(p)) {                                  // tensor-core path
     if (p.sub_splits == 1) { attn_mma_free(a, s, ring, r, p, ib, ie, ct); return; }
     const int per = kConsWarps / p.sub_splits;
@@ -2698,6 +2725,7 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
     bar_sync(1, kCons);
     const int4 ent = s.cur;
     if (ent.x < 0 || s.abort_flag) break;
+    MK_TRACE(a, s, ct, 6);
     const mk_task& t = s.tcache[qi];
     switch (t.op) {
       case MK_OP_GEMM:
@@ -2710,7 +2738,7 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
         run_gemm<F>(a, s, ring, r, t, worker, gw, ent.x, ct, n_tiles);
         break;
       case MK_OP_RMSNORM: run_rmsnorm(a, s, t, ent.y, ent.z, ct); break;
-      case MK_OP_ATTN_PARTIAL: run_attn_partial(a, s, ring, r, t, ent.y, ent.z, ct); break;
+      case MK_OP_ATTN_PARTIAL: run_attn_partial<F>(a, s, ring, r, t, ent.y, ent.z, ct); break;
       case MK_OP_ATTN_REDUCE: run_attn_reduce(a, s, t, ent.y, ent.z, ct); break;
       case MK_OP_SILU: run_silu(a, t, ct); break;
       case MK_OP_ARGMAX: run_argmax(a, s, t, ent.y, ent.z, ct); break;
@@ -2750,7 +2778,10 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
 #pragma unroll
         for (int i = 1; i < 6; ++i) rec[i] = s.tr[i];
         rec[6] = globaltimer();
-        rec[7] = n_exec;
+        // n_exec | sub-phase stamps as ns after the acquire (0: not reached)
+        const uint64_t d6 = s.tr[6] ? min(s.tr[6] - s.tr[2], uint64_t(0x3FFFFF)) : 0;
+        const uint64_t d7 = s.tr[7] ? min(s.tr[7] - s.tr[2], uint64_t(0x3FFFFF)) : 0;
+        rec[7] = (n_exec & 0xFFFFF) | (d6 << 20) | (d7 << 42);
       }
       mbar_arrive(&s.tq_empty[qi]);
     }
@@ -2964,7 +2995,11 @@ struct mk_handle {
 };
 
 static const void* kernel_for(int feat) {
-  // two instances: the plain CUDA-core graph, and everything else
+  // lean instances when the graph qualifies (kFeatLean), else the plain
+  // CUDA-core graph's instance or the general one
+  if (feat & kFeatLean)
+    return (feat & kFeatUmma) ? (const void*)megakernel<kFeatLean | kFeatUmma | kFeatKsplit>
+                              : (const void*)megakernel<kFeatLean | kFeatKsplit>;
   if ((feat & (kFeatUmma | kFeatKsplit)) == 0) return (const void*)megakernel<0>;
   return (const void*)megakernel<kFeatUmma | kFeatKsplit>;
 }
@@ -3333,6 +3368,24 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
         reinterpret_cast<const mk_gemm_params*>(static_cast<const uint8_t*>(g->params) + t.param_off);
     if (gp->body == MK_BODY_UMMA) h->feat |= kFeatUmma;
     if (gp->ksplit) h->feat |= kFeatKsplit;
+  }
+  {   // lean instance: every GEMM of one body kind (batch-1 GEMV, or all
+      // tcgen05) and only the one-warp-per-item tensor-core attention
+    bool lean = getenv("MK_NO_LEAN") == nullptr;
+    int n_umma = 0, n_gemv = 0;
+    for (int i = 0; i < g->n_tasks && lean; ++i) {
+      const mk_task& t = g->tasks[i];
+      const uint8_t* pb = static_cast<const uint8_t*>(g->params) + t.param_off;
+      if (t.op == MK_OP_GEMM) {
+        const mk_gemm_params* gp = reinterpret_cast<const mk_gemm_params*>(pb);
+        if (gp->body == MK_BODY_UMMA) ++n_umma;
+        else { ++n_gemv; lean = std::min(gp->T_M, gp->M) <= 1; }
+      } else if (t.op == MK_OP_ATTN_PARTIAL) {
+        const mk_attn_params* ap = reinterpret_cast<const mk_attn_params*>(pb);
+        lean = attn_mma_path(*ap) && ap->sub_splits == 1;
+      }
+    }
+    if (lean && !(n_umma && n_gemv)) h->feat |= kFeatLean;
   }
   h->kernel = kernel_for(h->feat);
   CK(cudaFuncSetAttribute(h->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));

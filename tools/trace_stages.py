@@ -68,6 +68,9 @@ def main():
         body = (rs[:, 4] - body_start) / 1e3
         skew = (rs[:, 5] - rs[:, 4]) / 1e3
         sig = (rs[:, 6] - rs[:, 5]) / 1e3
+        # sub-phases packed in word 7: consumers released / x rows loaded (ns after acquire)
+        rel = ((rs[:, 7] >> 20) & 0x3FFFFF) / 1e3
+        xld = ((rs[:, 7] >> 42) & 0x3FFFFF) / 1e3
         rows.append(dict(stage=key, units=len(rs),
                          start=(rs[:, 2].min() - t0) / 1e3, end=(rs[:, 6].max() - t0) / 1e3,
                          first_done=(rs[:, 6].min() - t0) / 1e3,
@@ -75,18 +78,20 @@ def main():
                          body_med=float(np.median(body)), body_max=float(body.max()),
                          body_min=float(body.min()),
                          skew_med=float(np.median(skew)), sig_med=float(np.median(sig)),
-                         sig_max=float(sig.max())))
+                         sig_max=float(sig.max()),
+                         rel_med=float(np.median(rel)),
+                         xld_med=float(np.median(xld[xld > 0])) if (xld > 0).any() else 0.0))
     total = (recs[:, 6].max() - t0) / 1e3
     print(f"total {total:.1f} us")
     hdr = ("stage", "units", "start", "end", "1st_done", "stage_med", "body_min", "body_med",
-           "body_max", "skew_med", "sig_med", "sig_max")
+           "body_max", "skew_med", "sig_med", "sig_max", "rel_med", "xld_med")
     print(" ".join(f"{h:>10}" for h in hdr))
     for r in rows:
         if r["stage"].startswith(("L0.", "L1.", "L17.", "L35.")) or not r["stage"].startswith("L"):
             print(f"{r['stage']:>10} {r['units']:>10} " + " ".join(
                 f"{r[k]:>10.2f}" for k in ("start", "end", "first_done", "stage_med", "body_min",
                                            "body_med", "body_max", "skew_med", "sig_med",
-                                           "sig_max")))
+                                           "sig_max", "rel_med", "xld_med")))
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump(dict(batch=args.batch, mode=args.mode, total_us=total, stages=rows, **info),
               open(args.out, "w"), indent=1)
