@@ -162,6 +162,9 @@ struct Smem {
   uint64_t job_full;
   int4 job;                         // {task, worker-in-task, first ring slot, 0}
   uint64_t tr[8];                   // phase stamps of the current unit (trace)
+  uint64_t xs_bar;                  // hoisted x / gamma staging (TMA bulk copies)
+  int xs_hoist;                     // the current unit's x rows (+ gamma) are in flight to u.xs
+  uint32_t xs_parity;               //   ... on this phase of xs_bar
   uint32_t tmem_base;
   // Descriptor cache: the mailbox warp copies every queued unit's task
   // descriptor and parameter block here, so no role reads them from global
@@ -580,34 +583,60 @@ __device__ __forceinline__ void dot8_acc(const float (&w)[8], const float (&x)[8
 // Stage rows [m0, m0+rows) of x (K wide) into s.u.xs, optionally applying
 // Qwen3RMSNorm (fp32 statistics, cast, gamma) -- the rms task fused into its
 // consumer GEMM.  Bit-identical to run_rmsnorm's output.
-__device__ void stage_x(Smem& s, const mk_gemm_params& p, int m0, int rows, int ct, bool trace) {
+__device__ void stage_x(const KArgs& a, Smem& s, const mk_gemm_params& p, int m0, int rows, int ct,
+                        bool trace) {
   const uint16_t* x = reinterpret_cast<const uint16_t*>(p.x);
   const int K = p.K;
   const bool norm = p.norm_gamma != nullptr;
   const uint16_t* gam = reinterpret_cast<const uint16_t*>(p.norm_gamma);
   constexpr int kSeg = 6;                  // K <= 6 * 2048 per thread pass
-  // gamma is static: issue its loads together with x's (one round trip)
-  uint4 gv[kSeg];
-#pragma unroll
-  for (int q = 0; q < kSeg; ++q) {
-    const int k = ct * 8 + q * kCons * 8;
-    gv[q] = (norm && k < K) ? *reinterpret_cast<const uint4*>(gam + k) : make_uint4(0, 0, 0, 0);
-  }
   float ss[kMaxNB];
 #pragma unroll
   for (int b = 0; b < kMaxNB; ++b) ss[b] = 0.f;
+  uint4 gv[kSeg];
+  if (s.xs_hoist) {
+    // consumer 0 bulk-copied the rows (and gamma, behind them) right after
+    // the dependency poll: only the wait and the sums of squares remain
+    mbar_wait(a, &s.xs_bar, s.xs_parity, -17);
+    const uint16_t* gs = s.u.xs + rows * K;
 #pragma unroll
-  for (int b = 0; b < kMaxNB; ++b) {
-    if (b < rows) {
+    for (int q = 0; q < kSeg; ++q) {
+      const int k = ct * 8 + q * kCons * 8;
+      gv[q] = (norm && k < K) ? *reinterpret_cast<const uint4*>(gs + k) : make_uint4(0, 0, 0, 0);
+    }
+    if (norm) {
+#pragma unroll
+      for (int b = 0; b < kMaxNB; ++b) {
+        if (b < rows) {
+          for (int k = ct * 8; k < K; k += kCons * 8) {
+            float f[8];
+            unpack8(*reinterpret_cast<const uint4*>(&s.u.xs[b * K + k]), f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) ss[b] = fmaf(f[e], f[e], ss[b]);
+          }
+        }
+      }
+    }
+  } else {
+    // gamma is static: issue its loads together with x's (one round trip)
+#pragma unroll
+    for (int q = 0; q < kSeg; ++q) {
+      const int k = ct * 8 + q * kCons * 8;
+      gv[q] = (norm && k < K) ? *reinterpret_cast<const uint4*>(gam + k) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int b = 0; b < kMaxNB; ++b) {
+      if (b < rows) {
 #pragma unroll 4
-      for (int k = ct * 8; k < K; k += kCons * 8) {
-        const uint4 v = ldg128_cg(x + size_t(m0 + b) * p.ldx + k);
-        *reinterpret_cast<uint4*>(&s.u.xs[b * K + k]) = v;
-        if (norm) {
-          float f[8];
-          unpack8(v, f);
+        for (int k = ct * 8; k < K; k += kCons * 8) {
+          const uint4 v = ldg128_cg(x + size_t(m0 + b) * p.ldx + k);
+          *reinterpret_cast<uint4*>(&s.u.xs[b * K + k]) = v;
+          if (norm) {
+            float f[8];
+            unpack8(v, f);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) ss[b] = fmaf(f[e], f[e], ss[b]);
+            for (int e = 0; e < 8; ++e) ss[b] = fmaf(f[e], f[e], ss[b]);
+          }
         }
       }
     }
@@ -1108,7 +1137,7 @@ __device__ void gemm_task(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
     cur_m = m;
     if constexpr (XS) {
       if (m != staged_m) {
-        stage_x(s, p, m * p.T_M, min(p.T_M, p.M - m * p.T_M), ct, a.trace != nullptr);
+        stage_x(a, s, p, m * p.T_M, min(p.T_M, p.M - m * p.T_M), ct, a.trace != nullptr);
         staged_m = m;
       }
     }
@@ -1197,7 +1226,7 @@ __device__ void gemm_task_ks(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
     cur_m = m;
     if constexpr (XS) {
       if (m != staged_m) {
-        stage_x(s, p, m * p.T_M, min(p.T_M, p.M - m * p.T_M), ct, a.trace != nullptr);
+        stage_x(a, s, p, m * p.T_M, min(p.T_M, p.M - m * p.T_M), ct, a.trace != nullptr);
         staged_m = m;
       }
     }
@@ -1716,13 +1745,16 @@ __device__ __forceinline__ void norm_rope8(const uint16_t* src, const uint16_t* 
                                            float (&out)[8]) {
   constexpr int LPT = HD / 8;
   constexpr int H2 = HD / 2;
+  const uint64_t pol = policy_evict_last();
   const uint4 xv = ldg128_cg(src + dl * 8);
-  const uint4 gv = *reinterpret_cast<const uint4*>(gam + dl * 8);
+  const uint4 gv = ldg128_hint(gam + dl * 8, pol);
   const int ci = (dl * 8) % H2;
-  const float4 c0 = *reinterpret_cast<const float4*>(cs + ci);
-  const float4 c1 = *reinterpret_cast<const float4*>(cs + ci + 4);
-  const float4 s0 = *reinterpret_cast<const float4*>(sn + ci);
-  const float4 s1 = *reinterpret_cast<const float4*>(sn + ci + 4);
+  const uint4 c0u = ldg128_hint(cs + ci, pol), c1u = ldg128_hint(cs + ci + 4, pol);
+  const uint4 s0u = ldg128_hint(sn + ci, pol), s1u = ldg128_hint(sn + ci + 4, pol);
+  const float4 c0 = make_float4(__uint_as_float(c0u.x), __uint_as_float(c0u.y), __uint_as_float(c0u.z), __uint_as_float(c0u.w));
+  const float4 c1 = make_float4(__uint_as_float(c1u.x), __uint_as_float(c1u.y), __uint_as_float(c1u.z), __uint_as_float(c1u.w));
+  const float4 s0 = make_float4(__uint_as_float(s0u.x), __uint_as_float(s0u.y), __uint_as_float(s0u.z), __uint_as_float(s0u.w));
+  const float4 s1 = make_float4(__uint_as_float(s1u.x), __uint_as_float(s1u.y), __uint_as_float(s1u.z), __uint_as_float(s1u.w));
   float f[8], g[8];
   unpack8(xv, f);
   unpack8(gv, g);
@@ -2310,8 +2342,10 @@ __device__ void attn_mma_free(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
 #pragma unroll
     for (int u = 0; u < 16; ++u) o[u][0] = o[u][1] = o[u][2] = o[u][3] = 0.f;
     const int nvalid = min(kAttnSplit, pos + 1 - t0);
+    const bool stamp = a.trace != nullptr && ct == 0 && s.tr[3] == 0;
     attn_mma_tokens(a, s, ring, p, b, pos, t0, nvalid, 0, kAttnSplit, kpos, true, warp, lane,
-                    o, m_run, l_run, trace, ph1, ph2);
+                    o, m_run, l_run, trace || stamp, ph1, ph2);
+    if (stamp) { s.tr[7] = ph1; s.tr[3] = ph2; }   // q norm+RoPE done / K,V slots ready
     __syncwarp();
     if (lane == 0) {
       mbar_arrive_cnt(&s.empty[kpos % kSlots], kConsWarps);
@@ -2687,6 +2721,7 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
                      n_exec = 0;
   uint64_t t_start = 0;
   uint32_t xs_k = 0, tb_k = 0;      // tcgen05 path: x-ring / accumulator-buffer counters
+  uint32_t xs_ph = 0;               // hoisted x staging: xs_bar phases used (consumer 0)
   for (;;) {
     const int qi = q % kTQ;
     // thread 0 takes the next unit and resolves its dependencies; the
@@ -2695,10 +2730,33 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
     if (ct == 0) {
       int4 ent = make_int4(-1, 0, 0, 0);
       if (mbar_wait(a, &s.tq_full[qi], (q / kTQ) & 1, -7)) ent = s.tq[qi];
+      int hoist = 0;
+      uint32_t xb = 0;
+      const void* xsrc = nullptr;
       if (ent.x >= 0) {
         const mk_task& t = s.tcache[qi];
         const int waits[2] = {t.wait0, t.wait1};
         uint32_t polls = 0;
+        if (t.op == MK_OP_GEMM) {
+          // a CUDA-core GEMM that stages its x rows: one m-tile of
+          // contiguous rows (+ the norm gamma) fits u.xs -> bulk-copy them
+          // into shared memory as soon as the dependency resolves (gamma,
+          // static, already now); the copy overlaps the op's code fetch
+          const mk_gemm_params& gp = *P<mk_gemm_params>(a, t);
+          if (gp.stage_x && gp.body != MK_BODY_UMMA && gp.M <= gp.T_M && gp.ldx == gp.K) {
+            xb = uint32_t(gp.M) * uint32_t(gp.K) * 2u;
+            const uint32_t gb = gp.norm_gamma ? uint32_t(gp.K) * 2u : 0u;
+            if (xb + gb <= uint32_t(kXsBytes) && (xb & 15u) == 0 && (gb & 15u) == 0) {
+              hoist = 1;
+              xsrc = gp.x;
+              if (gb) {
+                mbar_expect_tx(&s.xs_bar, gb);
+                bulk_g2s(reinterpret_cast<uint8_t*>(s.u.xs) + xb, gp.norm_gamma, gb, &s.xs_bar,
+                         policy_evict_last());
+              }
+            }
+          }
+        }
         if (a.trace) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) s.tr[i] = 0;
@@ -2718,7 +2776,15 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
         n_poll += polls;
         if (a.log) t_start = globaltimer();
         if (a.trace) s.tr[2] = globaltimer();
+        if (hoist) {
+          fence_proxy_async_global();     // generic-proxy writes of x -> TMA reads
+          mbar_arrive_expect_tx(&s.xs_bar, xb);
+          bulk_g2s_plain(s.u.xs, xsrc, xb, &s.xs_bar);
+        }
       }
+      s.xs_hoist = hoist;
+      s.xs_parity = xs_ph & 1u;
+      xs_ph += uint32_t(hoist);
       s.cur = ent;
       s.abort_flag = aborted(a) ? 1 : 0;
     }
@@ -2823,6 +2889,7 @@ __global__ void __launch_bounds__(kThreads, 1) megakernel(const __grid_constant_
     for (int i = 0; i < kXStagesMax; ++i) { mbar_init(&s.xfull[i], 1); mbar_init(&s.xempty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&s.tile_done[i], 1); mbar_init(&s.tmem_free[i], kConsWarps); }
     mbar_init(&s.job_full, 1);
+    mbar_init(&s.xs_bar, 1);
     fence_mbar_init();
     if (blockIdx.x == 0) atomicAdd(&a.stats[S_STEPS], 1ull);
   }

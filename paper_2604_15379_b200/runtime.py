@@ -429,7 +429,10 @@ def _default_lm_tile(spec: Qwen3Spec, batch: int, t_m: int | None = None,
 
 @dataclass
 class DeviceTrace:
-    """simulate()-shaped result of device runs (ref runtime.py:92-171)."""
+    """simulate()-shaped result of device runs (ref runtime.py:92-171).
+
+    ``to_json()`` / ``csv_row()`` emit the reference's record and CSV
+    columns (``report.py``), so ``comparison_table`` renders device runs."""
 
     mode: str
     batch: int
@@ -443,31 +446,69 @@ class DeviceTrace:
     dispatches: int
     counters: dict
     event_log: tuple
+    metrics: object = None
+    stage_costs: tuple = ()
+    estimated_time_s: float = 0.0
+    policy_notes: tuple = ()
+    model_fingerprint: tuple | None = None
+    fence_flush_lines: int = 0          # a simulator quantity: no device equivalent
+
+    def to_json(self) -> dict:
+        from .report import trace_to_json
+        return trace_to_json(self)
+
+    def csv_row(self, scenario_id: str) -> str:
+        from .report import trace_csv_row
+        return trace_csv_row(self, scenario_id)
 
 
 def run(g: TaskGraph, weights: Qwen3Weights, *, t_max: int, steps: int = 1,
         traversal=Traversal.M_MAJOR_WINDOWED,
         distribution=Distribution.M_TILE, sched: str = "per_die",
         keep_event_log: bool = True, fanout: bool = True,
-        topo=None) -> DeviceTrace:
-    """Execute ``steps`` decode steps of ``g`` on the GPU (drop-in for simulate)."""
+        topo=None, positions=None, ncu_csv: str | None = None) -> DeviceTrace:
+    """Execute ``steps`` decode steps of ``g`` on the GPU (drop-in for simulate).
+
+    ``positions``: the per-row context at the first step (default 0).
+    ``ncu_csv``: text of an ``ncu --csv --metrics`` capture of one of these
+    launches; its L2 / DRAM counters become the trace's metrics (else the
+    step's algorithmic bytes, L2 hit rate NaN)."""
+    from . import report
     mk = Megakernel(g, weights, t_max=t_max, traversal=traversal,
                     distribution=distribution, sched=sched, fanout=fanout,
                     topo=topo)
+    if positions is not None:
+        mk.set_positions(positions)
+    ctx0 = float(mk.positions().float().mean())
     cap = 0
     if keep_event_log:
         cap = 4 * (len(mk.lowered.units) * (g.machine.workers_per_xcd + 1)) + 1024
         mk.enable_log(cap)
-    for _ in range(steps):
-        mk.step()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * steps)]
+    for i in range(steps):
+        ev[2 * i].record()
+        mk.launch()
+        ev[2 * i + 1].record()
+        mk.sync()
+    secs = sum(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(steps)) / 1e3 / max(steps, 1)
     c = mk.counters()
     log = ()
     if keep_event_log:
         recs, _ = mk.read_log(cap)
         log = tuple(device_log_to_reference(mk, recs))
+    ctx = int(round(ctx0 + (steps + 1) / 2))        # mean attended context
+    metrics = report.metrics_from_ncu(ncu_csv) if ncu_csv else \
+        report.metrics_algorithmic(g, ctx, mk.spec.vocab)
+    m = g.model
     tr = DeviceTrace(g.mode, g.batch, traversal.value, distribution.value,
                      steps, c["fences"], c["global_atomics"], c["local_atomics"],
-                     c["polls"], c["dispatches"], c, log)
+                     c["polls"], c["dispatches"], c, log,
+                     metrics=metrics, stage_costs=report.stage_costs(g, ctx),
+                     estimated_time_s=secs,
+                     policy_notes=(f"sched={sched}", f"metrics={metrics.source}",
+                                   "time=measured_device_s_per_step",
+                                   f"workers_per_die={mk.lowered.workers}"),
+                     model_fingerprint=(m.hidden_dim, m.ffn_dim, m.num_layers, m.q_heads, m.kv_heads))
     mk.close()
     return tr
 
