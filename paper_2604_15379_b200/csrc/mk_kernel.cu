@@ -64,7 +64,15 @@ constexpr int kMaxSplits = 128;                 // split-KV splits per row
 constexpr int kMaxPieces = 512;                 // splits x token subsets
 constexpr int kXStagesMax = 16;                 // UMMA activation ring: up to 16 stages of
                                                 //   NT rows x 64 bf16 (128B-swizzled), TMA-fed
-constexpr int kTmemCols = 128;                  // 2 accumulator buffers x 64 columns
+// TMEM: 2 accumulator buffers (segments double-buffered) x 4 independent
+// accumulators x 64 columns.  The 4 MMAs of a K-chunk go to 4 different
+// accumulators: back-to-back skinny MMAs (N <= 64) into ONE accumulator are
+// bound by the dependent-accumulate latency (measured ~900 cycles per
+// chunk at N = 16 and N = 64 alike), not by the tensor pipe.
+constexpr int kAccs = 4;
+constexpr int kAccCols = 64;
+constexpr int kBufCols = kAccs * kAccCols;
+constexpr int kTmemCols = 2 * kBufCols;
 constexpr int kTQ = 32;                         // smem unit queue depth
 constexpr int kPBytes = 192;                    // param block bytes cached per queued unit
 constexpr int kPosRows = 256;                   // decode positions cached per CTA
@@ -1297,7 +1305,7 @@ __device__ __forceinline__ int umma_nt(const mk_gemm_params& p) {
 // (a single diverged lane would leave the other 31 parked at a convergence
 // barrier); lane 0 of each issues.  The per-chunk paths are kept short --
 // they pace the whole die task: ring / x-stage indices and phases advance
-// incrementally (x_stages is a power of two), smem descriptors are offsets
+// incrementally (stage index + phase bit), smem descriptors are offsets
 // of per-ring base descriptors.
 //
 // x-load warp (warp 3): for each job, TMA-loads the activation chunk of every
@@ -1305,10 +1313,11 @@ __device__ __forceinline__ int umma_nt(const mk_gemm_params& p) {
 // by the stage being released by the MMA that read it.
 __device__ void xload_warp(const KArgs& a, Smem& s) {
   const bool leader = (threadIdx.x & 31) == 0;
-  const int XS = a.x_stages;                 // power of two
-  const int xs_shift = __ffs(XS) - 1;
+  const int XS = a.x_stages;                 // x ring stages
   const uint32_t XB = uint32_t(a.x_stage_bytes);
-  uint32_t xs_load = 0, jq = 0;
+  uint32_t jq = 0;
+  int xl = 0;                                // x stage index / phase (any stage count)
+  uint32_t xph = 0;
   const bool no_tma = (a.debug & 16) != 0;
   for (;;) {
     if (!mbar_wait(a, &s.job_full, jq & 1, -15)) break;
@@ -1327,8 +1336,7 @@ __device__ void xload_warp(const KArgs& a, Smem& s) {
     while (lt.next(g)) {
       const int row = g.m * p.T_M;
       for (int c = g.c0; c < g.c1; ++c) {
-        const int xl = int(xs_load & uint32_t(XS - 1));
-        if (!mbar_spin(a, &s.xempty[xl], ((xs_load >> xs_shift) & 1) ^ 1, -13)) return;
+        if (!mbar_spin(a, &s.xempty[xl], xph ^ 1, -13)) return;
         if (leader) {
           if (no_tma) {                // diagnostics: no activation TMA
             mbar_arrive(&s.xfull[xl]);
@@ -1339,7 +1347,7 @@ __device__ void xload_warp(const KArgs& a, Smem& s) {
           }
         }
         __syncwarp();
-        ++xs_load;
+        if (++xl == XS) { xl = 0; xph ^= 1; }
       }
     }
   }
@@ -1350,11 +1358,11 @@ __device__ void xload_warp(const KArgs& a, Smem& s) {
 // release both through tcgen05.commit; one commit per segment to tile_done.
 __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
   const bool leader = (threadIdx.x & 31) == 0;
-  const int XS = a.x_stages;                 // power of two
-  const int xs_shift = __ffs(XS) - 1;
+  const int XS = a.x_stages;                 // x ring stages
   const uint32_t XB = uint32_t(a.x_stage_bytes);
   int ri = 0; uint32_t rph = 0;              // ring slot index / phase
-  uint32_t xs_mma = 0, tb_k = 0, jq = 0;
+  int xi = 0; uint32_t xph = 0;              // x stage index / phase
+  uint32_t tb_k = 0, jq = 0;
   unsigned long long w_full = 0, w_x = 0, w_tmem = 0, n_chunks = 0;
   // diagnostics flags read once: the per-chunk path paces the die task
   const bool prof = (a.debug & 4) != 0, no_mma = (a.debug & 8) != 0;
@@ -1366,50 +1374,79 @@ __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
     const int4 job = s.job;
     if (job.x < 0) break;
     const mk_gemm_params& p = *P<mk_gemm_params>(a, s.tcache[job.w]);
-    const uint32_t idesc = umma_idesc_bf16(128, umma_nt(p));
+    // Everything the UMMA issue path reads is made provably warp-uniform
+    // (values broadcast from lane 0 by shfl): the descriptors then live in
+    // uniform registers, instead of a per-instruction ELECT / R2UR
+    // waterfall around every UTCHMMA (measured ~120 cycles per MMA).
+    const uint32_t idesc = __shfl_sync(0xffffffffu, umma_idesc_bf16(128, umma_nt(p)), 0);
+    const uint32_t tmem0 = __shfl_sync(0xffffffffu, s.tmem_base, 0);
     // the job starts at the consumers' ring cursor (job.z)
-    ri = int(uint32_t(job.z) % kSlots);
-    rph = (uint32_t(job.z) / kSlots) & 1;
+    ri = __shfl_sync(0xffffffffu, int(uint32_t(job.z) % kSlots), 0);
+    rph = __shfl_sync(0xffffffffu, (uint32_t(job.z) / kSlots) & 1, 0);
     SegIter it;
     it.init(p, a.W, job.y);
     Seg sg;
-    while (it.next(sg)) {
+    for (;;) {
+      if (!__shfl_sync(0xffffffffu, it.next(sg) ? 1 : 0, 0)) break;
+      sg.c0 = __shfl_sync(0xffffffffu, sg.c0, 0);
+      sg.c1 = __shfl_sync(0xffffffffu, sg.c1, 0);
       const int buf = tb_k & 1;
-      if (!(prof ? mbar_wait_p(a, &s.tmem_free[buf], ((tb_k >> 1) & 1) ^ 1, -10, w_tmem)
-                 : mbar_spin(a, &s.tmem_free[buf], ((tb_k >> 1) & 1) ^ 1, -10))) return;
+      bool ok = prof ? mbar_wait_p(a, &s.tmem_free[buf], ((tb_k >> 1) & 1) ^ 1, -10, w_tmem)
+                     : mbar_spin(a, &s.tmem_free[buf], ((tb_k >> 1) & 1) ^ 1, -10);
+      if (!__all_sync(0xffffffffu, ok)) return;
       tc_fence_after();
-      const uint32_t d = s.tmem_base + uint32_t(buf * 64);
-      for (int c = sg.c0; c < sg.c1; ++c) {
-        if (prof) ++n_chunks;
-        const int xi = int(xs_mma & uint32_t(XS - 1));
+      const uint32_t d = tmem0 + uint32_t(buf * kBufCols);
+      int c = sg.c0;
+      // chunk pairs: one loop pass (waits, fences, issue setup) per 32 KiB
+      for (; !no_mma && c + 1 < sg.c1; c += 2) {
+        const int ri1 = ri + 1 == kSlots ? 0 : ri + 1;
+        const uint32_t rph1 = ri + 1 == kSlots ? rph ^ 1 : rph;
+        const int xi1 = xi + 1 == XS ? 0 : xi + 1;
+        const uint32_t xph1 = xi + 1 == XS ? xph ^ 1 : xph;
         if (prof) {
-          if (!mbar_wait_p(a, &s.full[ri], rph, -11, w_full)) return;
-          if (!mbar_wait_p(a, &s.xfull[xi], (xs_mma >> xs_shift) & 1, -12, w_x)) return;
+          n_chunks += 2;
+          ok = mbar_wait_p(a, &s.full[ri], rph, -11, w_full) && mbar_wait_p(a, &s.xfull[xi], xph, -12, w_x) &&
+               mbar_wait_p(a, &s.full[ri1], rph1, -11, w_full) && mbar_wait_p(a, &s.xfull[xi1], xph1, -12, w_x);
         } else {
-          if (!mbar_spin(a, &s.full[ri], rph, -11)) return;
-          if (!mbar_spin(a, &s.xfull[xi], (xs_mma >> xs_shift) & 1, -12)) return;
+          ok = mbar_spin(a, &s.full[ri], rph, -11) && mbar_spin(a, &s.xfull[xi], xph, -12) &&
+               mbar_spin(a, &s.full[ri1], rph1, -11) && mbar_spin(a, &s.xfull[xi1], xph1, -12);
         }
+        if (!__all_sync(0xffffffffu, ok)) return;
         tc_fence_after();
-        if (leader) {
-          if (no_mma) {                  // diagnostics: no MMA, release at once
+        umma_chunk8(d, adesc0 + uint64_t(ri * (kSlotBytes >> 4)), bdesc0 + uint64_t(xi * (XB >> 4)),
+                    adesc0 + uint64_t(ri1 * (kSlotBytes >> 4)), bdesc0 + uint64_t(xi1 * (XB >> 4)),
+                    idesc, c != sg.c0 ? 1u : 0u, &s.empty[ri], &s.empty[ri1], kConsWarps - 1,
+                    &s.xempty[xi], &s.xempty[xi1]);
+        __syncwarp();
+        ri = ri1 + 1 == kSlots ? 0 : ri1 + 1;
+        rph = ri1 + 1 == kSlots ? rph1 ^ 1 : rph1;
+        xi = xi1 + 1 == XS ? 0 : xi1 + 1;
+        xph = xi1 + 1 == XS ? xph1 ^ 1 : xph1;
+      }
+      for (; c < sg.c1; ++c) {
+        if (prof) ++n_chunks;
+        if (prof) {
+          ok = mbar_wait_p(a, &s.full[ri], rph, -11, w_full) && mbar_wait_p(a, &s.xfull[xi], xph, -12, w_x);
+        } else {
+          ok = mbar_spin(a, &s.full[ri], rph, -11) && mbar_spin(a, &s.xfull[xi], xph, -12);
+        }
+        if (!__all_sync(0xffffffffu, ok)) return;
+        tc_fence_after();
+        if (no_mma) {                    // diagnostics: no MMA, release at once
+          if (leader) {
             mbar_arrive_cnt(&s.empty[ri], kConsWarps);
             mbar_arrive(&s.xempty[xi]);
-          } else {
-            const uint64_t ad = adesc0 + uint64_t(ri * (kSlotBytes >> 4));
-            const uint64_t bd = bdesc0 + uint64_t(xi * (XB >> 4));
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)   // UMMA_K = 16 bf16 = 32 B along the swizzled row
-              umma_bf16(d, ad + uint64_t(2 * kk), bd + uint64_t(2 * kk), idesc, (c != sg.c0 || kk != 0));
-            // ring slot: 8 arrivals (one per GEMV consumer warp); 7 now, the
-            // eighth from the commit when the MMAs have read the slot
-            mbar_arrive_cnt(&s.empty[ri], kConsWarps - 1);
-            umma_commit(&s.empty[ri]);
-            umma_commit(&s.xempty[xi]);
           }
+        } else {
+          // UMMA_K = 16 bf16 = 32 B along the swizzled row, 4 per 64-wide chunk;
+          // ring slot: 8 arrivals (one per GEMV consumer warp), 7 plain, the
+          // eighth from the commit when the MMAs have read the slot
+          umma_chunk4(d, adesc0 + uint64_t(ri * (kSlotBytes >> 4)), bdesc0 + uint64_t(xi * (XB >> 4)),
+                      idesc, c != sg.c0 ? 1u : 0u, &s.empty[ri], kConsWarps - 1, &s.xempty[xi]);
         }
         __syncwarp();
         if (++ri == kSlots) { ri = 0; rph ^= 1; }
-        ++xs_mma;
+        if (++xi == XS) { xi = 0; xph ^= 1; }
       }
       if (leader) {
         if (no_mma) mbar_arrive(&s.tile_done[buf]);
@@ -1427,9 +1464,37 @@ __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
 
 // Epilogue of 16 accumulator columns (batch rows 16j..16j+15) of weight row
 // `row` (TMEM lane): residual / interleaved SiLU / logits + running argmax.
+// 16 accumulator columns (batch rows 16j..) of TMEM lane quadrant q: the
+// sum of the kAccs independent accumulators, in accumulator order.
+__device__ __forceinline__ void tmem_acc16(uint32_t tmem_base, int q, int buf, int j, float (&v)[16]) {
+  const uint32_t t0 = tmem_base + (uint32_t(32 * q) << 16) + uint32_t(buf * kBufCols + 16 * j);
+  tmem_ld16(t0, v);
+#pragma unroll
+  for (int k = 1; k < kAccs; ++k) {
+    float w[16];
+    tmem_ld16(t0 + uint32_t(k * kAccCols), w);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] += w[i];
+  }
+}
+
+// Residual operands of one 16-column group (batch rows 16j..16j+15 of
+// weight row `row`), loaded ahead of the accumulator so their round trip
+// overlaps the MMA / piece wait.
+__device__ __forceinline__ void umma_res16(const mk_gemm_params& p, int m0, int rows_m, int col,
+                                           int j, float (&rv)[16]) {
+  const uint16_t* res = reinterpret_cast<const uint16_t*>(p.res);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int bi = 16 * j + i;
+    rv[i] = (p.epilogue == MK_EPI_RESIDUAL && bi < rows_m)
+                ? bf2f(ldg16_cg(res + size_t(m0 + bi) * p.ldres + col)) : 0.f;
+  }
+}
+
 __device__ __forceinline__ void umma_epi16(Smem& s, const mk_gemm_params& p, int m0, int rows_m,
                                            int out_col0, int row, int q, int lane, int cw, int j,
-                                           const float (&v)[16]) {
+                                           const float (&v)[16], const float* rpre = nullptr) {
   if (p.epilogue == MK_EPI_LOGITS) {
     float* y = reinterpret_cast<float*>(p.y);
     const int col = out_col0 + row;
@@ -1465,14 +1530,13 @@ __device__ __forceinline__ void umma_epi16(Smem& s, const mk_gemm_params& p, int
     }
   } else {
     uint16_t* y = reinterpret_cast<uint16_t*>(p.y);
-    const uint16_t* res = reinterpret_cast<const uint16_t*>(p.res);
     const int col = out_col0 + row;
     float rv[16];
+    if (rpre) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int bi = 16 * j + i;
-      rv[i] = (p.epilogue == MK_EPI_RESIDUAL && bi < rows_m)
-                  ? bf2f(ldg16_cg(res + size_t(m0 + bi) * p.ldres + col)) : 0.f;
+      for (int i = 0; i < 16; ++i) rv[i] = rpre[i];
+    } else {
+      umma_res16(p, m0, rows_m, col, j, rv);
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -1502,6 +1566,7 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
     const int m0 = g.m * p.T_M;
     const int rows_m = min(p.T_M, p.M - m0);
     const int buf = tb_k & 1;
+    const bool whole = g.c0 == 0 && g.c1 == chunks;
     {
       const long long t0 = (a.debug & 4) ? clock64() : 0;
       mbar_wait_warp(a, &s.tile_done[buf], (tb_k >> 1) & 1, -14);
@@ -1510,12 +1575,12 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
     tc_fence_after();
     const int row = 32 * q + lane;        // weight row inside the tile
     const int out_col0 = p.y_col0 + g.n * p.T_N;
-    const bool whole = g.c0 == 0 && g.c1 == chunks;
     if (whole) {
       for (int j = half; j < NT / 16; j += 2) {
-        float v[16];
-        tmem_ld16(s.tmem_base + (uint32_t(32 * q) << 16) + uint32_t(buf * 64 + 16 * j), v);
-        umma_epi16(s, p, m0, rows_m, out_col0, row, q, lane, cw, j, v);
+        float rv[16], v[16];
+        umma_res16(p, m0, rows_m, out_col0 + row, j, rv);
+        tmem_acc16(s.tmem_base, q, buf, j, v);
+        umma_epi16(s, p, m0, rows_m, out_col0, row, q, lane, cw, j, v, rv);
       }
       tc_fence_before();
       __syncwarp();
@@ -1523,44 +1588,73 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
       ++tb_k;
       continue;
     }
-    // partial piece: TMEM -> piece slot, release the accumulator early
-    float* mine = piece_ptr(p, w_in_task, g.first ? 0 : 1);
-    for (int j = half; j < NT / 16; j += 2) {
-      float v[16];
-      tmem_ld16(s.tmem_base + (uint32_t(32 * q) << 16) + uint32_t(buf * 64 + 16 * j), v);
+    // K-split tile.  Its owner is the worker holding the tile's first chunk
+    // (pi.first_w): that segment is the owner's LAST segment, so it is
+    // streamed last and the owner reduces while nothing else of its range
+    // is pending.  Every other piece goes TMEM -> piece slot -> release
+    // signal (no round trip waited on); the owner keeps its own partial in
+    // TMEM, waits for the n-1 signals, and sums all pieces in piece order
+    // (first_w, first_w+1, ...: deterministic, arrival-order independent).
+    const PieceInfo pi = tile_pieces(p, a.W, g.tile);
+    if (w_in_task != pi.first_w) {
+      float* mine = piece_ptr(p, w_in_task, g.first ? 0 : 1);
+      for (int j = half; j < NT / 16; j += 2) {
+        float v[16];
+        tmem_acc16(s.tmem_base, q, buf, j, v);
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (16 * j + i < rows_m) __stcg(mine + (16 * j + i) * 128 + row, v[i]);
+        for (int i = 0; i < 16; ++i)
+          if (16 * j + i < rows_m) __stcg(mine + (16 * j + i) * 128 + row, v[i]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s.tmem_free[buf]);
+      ++tb_k;
+      bar_sync(2, kCons);
+      if (ct == 0) {                        // cumulative release of the CTA's stores
+        fence_acq_rel_gpu();
+        red_release_add(&a.sub_ctr[p.tile_ctr0 + g.tile], 1u);
+      }
+      continue;
+    }
+    // owner: wait for the n-1 other pieces (their signals were sent while
+    // this worker streamed its own segment), then per column group: residual
+    // operands and up to three pieces in flight together, own partial from
+    // TMEM, sum in piece order, epilogue; the accumulator is released last
+    if (ct == 0) {
+      if (a.trace) s.tr[7] = globaltimer();          // own accumulator ready
+      const uint32_t target = uint32_t(pi.n - 1) * a.epoch;
+      Spin sp;
+      while ((int32_t)(ld_acquire(&a.sub_ctr[p.tile_ctr0 + g.tile]) - target) < 0)
+        if (!sp.ok(a, -18)) break;
+      if (a.trace) s.tr[6] = globaltimer();          // the other pieces arrived
+    }
+    bar_sync(2, kCons);
+    for (int j = half; j < NT / 16; j += 2) {
+      float rv[16], v[16];
+      umma_res16(p, m0, rows_m, out_col0 + row, j, rv);
+      tmem_acc16(s.tmem_base, q, buf, j, v);
+      for (int w0 = pi.first_w + 1; w0 <= pi.last_w; w0 += 3) {
+        float t[3][16];
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const int w = w0 + u;
+          const bool on = w <= pi.last_w && !pi.empty(w);
+          const float* src = piece_ptr(p, on ? w : pi.first_w, 0);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            t[u][i] = (on && 16 * j + i < rows_m) ? __ldcg(src + (16 * j + i) * 128 + row) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] += t[u][i];
+      }
+      umma_epi16(s, p, m0, rows_m, out_col0, row, q, lane, cw, j, v, rv);
     }
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&s.tmem_free[buf]);
     ++tb_k;
-    const PieceInfo pi = tile_pieces(p, a.W, g.tile);
-    __threadfence();
-    bar_sync(2, kCons);
-    if (ct == 0) {
-      const uint32_t old = atom_acq_rel_add(&a.sub_ctr[p.tile_ctr0 + g.tile], 1u);
-      s.epi_last = (old + 1 == uint32_t(pi.n) * a.epoch) ? 1 : 0;
-    }
-    bar_sync(2, kCons);
-    const int last = s.epi_last;
-    bar_sync(2, kCons);                   // epi_last reusable by the next segment
-    if (!last) continue;
-    __threadfence();
-    for (int j = half; j < NT / 16; j += 2) {
-      float v[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = 0.f;
-      for (int w = pi.first_w; w <= pi.last_w; ++w) {
-        if (pi.empty(w)) continue;
-        const float* src = piece_ptr(p, w, w == pi.first_w ? pi.slot0 : 0);
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (16 * j + i < rows_m) v[i] += __ldcg(src + (16 * j + i) * 128 + row);
-      }
-      umma_epi16(s, p, m0, rows_m, out_col0, row, q, lane, cw, j, v);
-    }
   }
 }
 
@@ -1689,6 +1783,63 @@ __device__ float block_sum(Smem& s, float v, int ct) {
 __device__ void run_rmsnorm(const KArgs& a, Smem& s, const mk_task& t, int ib, int ie, int ct) {
   const mk_norm_params& p = *P<mk_norm_params>(a, t);
   const uint16_t* gam = reinterpret_cast<const uint16_t*>(p.gamma);
+  constexpr int kRegChunks = 16;     // rows up to 16 * 256 wide stay in registers
+  if (p.d <= kRegChunks * 256) {
+    // one warp per row: the row and gamma are loaded in one round trip and
+    // kept in registers, the statistics reduced by shuffles (no CTA barrier)
+    const int warp = ct >> 5, lane = ct & 31;
+    const uint64_t pol = policy_evict_last();
+    for (int b = ib + warp; b < ie; b += kConsWarps) {
+      const uint16_t* src = p.embed ? reinterpret_cast<const uint16_t*>(p.embed) + size_t(p.tokens[b]) * p.d
+                                    : reinterpret_cast<const uint16_t*>(p.x) + size_t(b) * p.d;
+      uint16_t* xs = p.x_store ? reinterpret_cast<uint16_t*>(p.x_store) + size_t(b) * p.d : nullptr;
+      uint4 xv[kRegChunks], gv[kRegChunks];
+#pragma unroll
+      for (int i = 0; i < kRegChunks; ++i) {
+        const int k = lane * 8 + i * 256;
+        const bool on = k < p.d;
+        xv[i] = on ? ldg128_cg(src + k) : make_uint4(0, 0, 0, 0);
+        gv[i] = (on && !p.fused) ? ldg128_hint(gam + k, pol) : make_uint4(0, 0, 0, 0);
+      }
+      if (p.fused) {            // consumer GEMM normalises; keep only the gather
+        if (xs) {
+#pragma unroll
+          for (int i = 0; i < kRegChunks; ++i)
+            if (lane * 8 + i * 256 < p.d) *reinterpret_cast<uint4*>(xs + lane * 8 + i * 256) = xv[i];
+        }
+        continue;
+      }
+      float ss = 0.f;
+#pragma unroll
+      for (int i = 0; i < kRegChunks; ++i) {
+        float f[8];
+        unpack8(xv[i], f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ss = fmaf(f[e], f[e], ss);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+      const float rs = rsqrtf(ss / float(p.d) + p.eps);
+      uint16_t* y = reinterpret_cast<uint16_t*>(p.y) + size_t(b) * p.d;
+#pragma unroll
+      for (int i = 0; i < kRegChunks; ++i) {
+        const int k = lane * 8 + i * 256;
+        if (k >= p.d) continue;
+        float f[8], g[8];
+        unpack8(xv[i], f);
+        unpack8(gv[i], g);
+        uint16_t o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float xn = bf2f(f2bf(f[e] * rs));   // hidden_states.to(input_dtype)
+          o[e] = f2bf(g[e] * xn);                   // weight * hidden_states
+        }
+        *reinterpret_cast<uint4*>(y + k) = *reinterpret_cast<uint4*>(o);
+        if (xs) *reinterpret_cast<uint4*>(xs + k) = xv[i];
+      }
+    }
+    return;
+  }
   for (int b = ib; b < ie; ++b) {
     const uint16_t* src;
     if (p.embed) src = reinterpret_cast<const uint16_t*>(p.embed) + size_t(p.tokens[b]) * p.d;
@@ -3326,8 +3477,8 @@ static int build_tmaps(mk_handle* h, const mk_graph_desc* g) {
     any = true;
   }
   h->x_stage_bytes = max_nt * 128;
-  int xs = 1;                                       // power of two stages
-  while (xs * 2 <= kXStagesMax && (xs * 2) * h->x_stage_bytes <= kXsBytes) xs *= 2;
+  int xs = 1;                                       // as many stages as fit
+  xs = std::max(1, std::min(kXStagesMax, kXsBytes / h->x_stage_bytes));
   h->x_stages = xs;
   if (any) {
     CK(cudaMalloc(&h->d_tmaps, maps.size() * sizeof(CUtensorMap)));

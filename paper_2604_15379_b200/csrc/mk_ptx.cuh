@@ -266,6 +266,74 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
       :: "r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate) : "memory");
 }
+// One K-chunk (4 x UMMA_K = 16) of the skinny GEMM into 4 independent
+// accumulators (columns d, d+64, d+128, d+192), issued by the whole warp
+// in one convergent block: elect.sync picks the issuing lane inside the asm
+// (no divergent C++ branch around the MMAs, so the operands stay in
+// uniform registers); then `arrivals` plain arrivals on `slot_bar` and a
+// commit to it and to `x_bar` (both complete when the MMAs have read smem).
+__device__ __forceinline__ void umma_chunk4(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc,
+                                            uint32_t accumulate, uint64_t* slot_bar, uint32_t arrivals,
+                                            uint64_t* x_bar) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      ".reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      ".reg .b32 e1, e2, e3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.s64 a1, %1, 2; add.s64 a2, %1, 4; add.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2; add.s64 b2, %2, 4; add.s64 b3, %2, 6;\n\t"
+      "add.u32 e1, %0, 64; add.u32 e2, %0, 128; add.u32 e3, %0, 192;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [e1], a1, b1, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [e2], a2, b2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [e3], a3, b3, %3, p;\n\t"
+      "@e mbarrier.arrive.shared::cta.b64 _, [%5], %6;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t}"
+      :: "r"(d_tmem), "l"(a0), "l"(b0), "r"(idesc), "r"(accumulate), "r"(smem_u32(slot_bar)),
+         "r"(arrivals), "r"(smem_u32(x_bar))
+      : "memory");
+}
+
+// Two K-chunks in one block (8 MMAs): chunk 0 on (a0, b0) releasing
+// slot0 / x0, chunk 1 on (a1, b1) releasing slot1 / x1.
+__device__ __forceinline__ void umma_chunk8(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint64_t a1,
+                                            uint64_t b1, uint32_t idesc, uint32_t accumulate,
+                                            uint64_t* slot0, uint64_t* slot1, uint32_t arrivals,
+                                            uint64_t* x0, uint64_t* x1) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t"
+      ".reg .b64 c1, c2, c3, d1, d2, d3, f1, f2, f3, g1, g2, g3;\n\t"
+      ".reg .b32 e1, e2, e3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "setp.eq.b32 t, 0, 0;\n\t"
+      "add.u32 e1, %0, 64; add.u32 e2, %0, 128; add.u32 e3, %0, 192;\n\t"
+      "add.s64 c1, %1, 2; add.s64 c2, %1, 4; add.s64 c3, %1, 6;\n\t"
+      "add.s64 d1, %2, 2; add.s64 d2, %2, 4; add.s64 d3, %2, 6;\n\t"
+      "add.s64 f1, %3, 2; add.s64 f2, %3, 4; add.s64 f3, %3, 6;\n\t"
+      "add.s64 g1, %4, 2; add.s64 g2, %4, 4; add.s64 g3, %4, 6;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [e1], c1, d1, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [e2], c2, d2, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [e3], c3, d3, %5, p;\n\t"
+      "@e mbarrier.arrive.shared::cta.b64 _, [%7], %9;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %4, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [e1], f1, g1, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [e2], f2, g2, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [e3], f3, g3, %5, t;\n\t"
+      "@e mbarrier.arrive.shared::cta.b64 _, [%8], %9;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%11];\n\t}"
+      :: "r"(d_tmem), "l"(a0), "l"(b0), "l"(a1), "l"(b1), "r"(idesc), "r"(accumulate),
+         "r"(smem_u32(slot0)), "r"(smem_u32(slot1)), "r"(arrivals), "r"(smem_u32(x0)),
+         "r"(smem_u32(x1))
+      : "memory");
+}
+
 // arrive on an mbarrier once all previously issued tcgen05.mma of this thread complete
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"

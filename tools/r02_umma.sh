@@ -1,7 +1,7 @@
 #!/bin/bash
 # isolate the tcgen05 chunk-rate limiter: one die task per die, flags:
 # 0 normal, 2 no weight TMA, 16 no activation TMA, 18 neither, 8 no MMA, 4 wait counters
-O=gpurun_out/r02_umma
+O=gpurun_out/r02b_umma_flags
 mkdir -p $O
 python - <<'PY' > $O/umma_flags.log 2>&1
 import sys, json

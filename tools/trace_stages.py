@@ -35,6 +35,8 @@ def main():
     ap.add_argument("--t-m", type=int, default=None)
     ap.add_argument("--no-ksplit", action="store_true")
     ap.add_argument("--out", default="gpurun_out/trace.json")
+    ap.add_argument("--detail", action="append", default=[],
+                    help="stage key (e.g. L17.qkv): per-worker rows of that stage")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     mk, model, spec, info = bench.build(args, 0)
@@ -47,8 +49,10 @@ def main():
     mk.sync()
     tr = mk.read_trace()
     names = mk.lowered.task_names
+    gw_of = np.repeat(np.arange(tr.shape[0]), tr.shape[1])
     recs = tr.reshape(-1, 8)
-    recs = recs[recs[:, 7] > 0]
+    keep = recs[:, 7] > 0
+    recs, gw_of = recs[keep], gw_of[keep]
     t0 = int(recs[:, 2].min())
     by = collections.OrderedDict()
     order = []
@@ -92,6 +96,31 @@ def main():
                 f"{r[k]:>10.2f}" for k in ("start", "end", "first_done", "stage_med", "body_min",
                                            "body_med", "body_max", "skew_med", "sig_med",
                                            "sig_max", "rel_med", "xld_med")))
+    W = mk.lowered.workers
+    for key in args.detail:
+        sel = [i for i in range(len(recs))
+               if names[int(recs[i, 0] & 0xFFFFFFFF)].startswith(key + ".")]
+        if not sel:
+            continue
+        t_first = min(int(recs[i, 2]) for i in sel)
+        rows_d = []
+        for i in sel:
+            r = recs[i].astype(np.int64)
+            bs = r[3] if r[3] > 0 else r[2]
+            rows_d.append((gw_of[i] // W, gw_of[i] % W, (r[2] - t_first) / 1e3, (bs - r[2]) / 1e3,
+                           (r[4] - bs) / 1e3, (r[6] - t_first) / 1e3,
+                           ((r[7] >> 20) & 0x3FFFFF) / 1e3, ((r[7] >> 42) & 0x3FFFFF) / 1e3,
+                           names[int(r[0] & 0xFFFFFFFF)]))
+        rows_d.sort(key=lambda x: -x[4])
+        print(f"-- {key}: slowest bodies (die, worker, acquired, stage, body, signalled, "
+              "stamp6, stamp7 [after acquire], task)")
+        for d in rows_d[:12]:
+            print("   die %d w %3d  acq %6.2f  stage %5.2f  body %6.2f  sig %6.2f  s6 %6.2f  s7 %6.2f  %s" % d)
+        for die in sorted({d[0] for d in rows_d}):
+            b = np.array([d[4] for d in rows_d if d[0] == die])
+            print(f"   die {die}: n={len(b)} body med {np.median(b):.2f} max {b.max():.2f}")
+        wb = sorted(rows_d, key=lambda x: (x[0], x[1]))
+        print("   body by worker:", " ".join(f"{d[4]:.0f}" for d in wb))
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump(dict(batch=args.batch, mode=args.mode, total_us=total, stages=rows, **info),
               open(args.out, "w"), indent=1)
