@@ -31,7 +31,7 @@ import os
 from dataclasses import dataclass, field
 
 from . import _lib as L
-from .taskgraph import OpKind, TaskGraph, TaskLevel
+from .taskgraph import OpKind, TaskGraph, TaskLevel, adopt_graph
 from .traversal import Distribution, Traversal
 
 
@@ -155,7 +155,9 @@ def _ptr(t, elem_offset=0):
 
 
 def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
-    """Lower ``g`` against device buffers ``bufs`` (a runtime.DeviceState)."""
+    """Lower ``g`` against device buffers ``bufs`` (a runtime.DeviceState).
+    ``g`` may come from this package's builder or the reference's."""
+    g = adopt_graph(g)
     B = g.batch
     d, F, hd = spec.hidden, spec.ffn, spec.head_dim
     per_die = opts.sched_mode == L.SCHED_PER_DIE

@@ -32,7 +32,7 @@ from . import _lib as L
 from .lowering import PIECE_FLOATS, LoweringOptions, lower
 from .analytics import UMMA_MIN_BATCH, default_t_m
 from .machine import b200_from_probe
-from .taskgraph import OpKind, TaskGraph, TaskLevel
+from .taskgraph import OpKind, TaskGraph, TaskLevel, adopt_graph
 from .traversal import Distribution, Traversal
 from .lowering import is_umma_tile
 from .weights import (Qwen3Spec, Qwen3Weights, hash_uniform, pack_gate_up_fused,
@@ -122,6 +122,7 @@ class DeviceState:
 def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
                 amax_slots: int, device="cuda", split: int | None = None,
                 keep_logits: bool = True) -> DeviceState:
+    g = adopt_graph(g)
     sp = weights.spec
     B = g.batch
     dev = torch.device(device)
@@ -135,7 +136,9 @@ def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
     chiplet = g.mode == "chiplet"
     X = g.machine.num_xcds
     bf = dict(device=dev, dtype=torch.bfloat16)
-    n_layers = len(g.buffers)
+    # layers from the graph's stages (a reference-built TaskGraph carries no
+    # buffer table: ref taskgraph.py:135-145)
+    n_layers = max((s.layer for s in g.stages), default=-1) + 1
     for li in range(n_layers):
         Lw = w.layers[li]
         qkv = torch.cat((Lw["q"], Lw["k"], Lw["v"]), 0)
@@ -210,7 +213,7 @@ class Megakernel:
         self.lib = L.load()
         torch.cuda.set_device(device)
         self.device = device
-        self.graph = g
+        self.graph = g = adopt_graph(g)
         self.spec = weights.spec
         if topo is None:
             topo = probe(device)

@@ -153,6 +153,27 @@ class TaskGraph:
         return idx[task_id]
 
 
+def adopt_graph(g) -> "TaskGraph":
+    """This module's TaskGraph for ``g``, which may have been built by the
+    reference package itself (``chipletsim``, same field names, its own enum
+    classes: ref taskgraph.py:46-145).  Enum members are re-keyed by value;
+    payloads are used by attribute, so they pass through unchanged.  The
+    device lowering calls this first, so a graph built by either builder
+    lowers to the same descriptors."""
+    if isinstance(g, TaskGraph) and all(isinstance(t.op_kind, OpKind) for t in g.tasks):
+        return g
+    tasks = tuple(Task(t.id, TaskLevel(t.level.value), OpKind(t.op_kind.value),
+                       tuple(t.wait_events), t.signal_event, t.xcd_binding,
+                       t.gemm_shape, t.tile_shape, t.work, t.stage, t.flops)
+                  for t in g.tasks)
+    events = {k: Event(e.id, e.required_count, tuple(e.downstream_tasks))
+              for k, e in g.events.items()}
+    stages = tuple(StageRecord(s.index, s.layer, s.name, OpKind(s.op_kind.value),
+                               tuple(s.task_ids), s.event_id, s.flops) for s in g.stages)
+    return TaskGraph(tasks, events, stages, g.machine, g.model, g.batch, g.mode,
+                     tuple(g.op_counts), tuple(g.notes), tuple(getattr(g, "buffers", ())))
+
+
 STANDARD_TILE_PROFILE = {
     OpKind.QKV_PROJ: (16, 64, 256),
     OpKind.O_PROJ_RESIDUAL: (16, 16, 256),

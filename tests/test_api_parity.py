@@ -100,3 +100,37 @@ def test_schedules_match_reference():
         if "json" in c:
             assert doc == c["json"], c
         assert sha(doc) == c["sha256"], c
+
+
+PAYLOADS = _load("payloads.json")
+
+
+@pytest.mark.parametrize("case", PAYLOADS, ids=lambda c: f"{c['machine']}-{c['model']}-{c['mode']}-b{c['batch']}")
+def test_payloads_and_flops_match_reference(case):
+    """Work payloads, per-task flops and stage flops -- the graph content
+    graph_to_json omits -- equal the reference's (oracle/gen_extra_golden.py)."""
+    from oracle.gen_extra_golden_doc import digest, payload_doc
+    g = build_decoder_layer(model_preset(case["model"]), machine_of(case["machine"]),
+                            case["mode"], case["batch"], layers=case["layers"])
+    assert len(g.tasks) == case["n_tasks"]
+    assert digest(payload_doc(g)) == case["sha256"]
+
+
+def test_graph_error_messages_match_reference():
+    """Every GraphError path of validate_graph / build_decoder_layer raises
+    the reference's message (ref taskgraph.py:371-378, 555-612)."""
+    from oracle.graph_mutations import BUILD_ERRORS, MUTATIONS
+    from paper_2604_15379_b200 import GraphError
+    want = _load("graph_errors.json")
+    mach = preset("toy")
+    base = build_decoder_layer(model_preset("toy"), mach, "chiplet", 2, layers=2)
+    validate_graph(base)
+    for name, fn in MUTATIONS.items():
+        with pytest.raises(GraphError) as ei:
+            validate_graph(fn(base))
+        assert str(ei.value) == want[name], name
+    for name, kw in BUILD_ERRORS.items():
+        with pytest.raises(GraphError) as ei:
+            build_decoder_layer(model_preset("toy"), mach, kw["mode"], kw["batch"],
+                                layers=kw["layers"])
+        assert str(ei.value) == want[name], name

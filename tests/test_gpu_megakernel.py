@@ -443,3 +443,43 @@ def test_pass_synchronous_attention_matches_oracle(topo, machine, wpi, monkeypat
     worst, _ = _decode_vs_oracle(mk, w, B, steps=70, t_max=160)
     mk.close()
     assert worst < RTOL
+
+
+def test_run_is_a_simulate_dropin_with_reference_records(topo, machine):
+    """runtime.run() -- the simulate() replacement -- on a graph built by the
+    package API: the event log comes back in the reference's (time, actor,
+    action, task) shape through device_log_to_reference (ref
+    runtime.py:301-417: every task dispatched, started after its dispatch and
+    completed after it started), and the trace serialises to the reference's
+    SimTrace.to_json keys / CSV columns (tests/golden/reports.json) and
+    renders in comparison_table next to the flat-scheduler run."""
+    from paper_2604_15379_b200 import report
+    from paper_2604_15379_b200.runtime import run
+    from paper_2604_15379_b200.weights import Qwen3Spec, Qwen3Weights
+    gold = json.load(open(os.path.join(GOLD, "reports.json")))
+    w = Qwen3Weights.random(Qwen3Spec.toy(), seed=16)
+    traces = {}
+    for mode, sched in (("chiplet", "per_die"), ("standard", "flat")):
+        g = _toy_graph(machine, mode, 2)
+        tr = run(g, w, t_max=64, steps=2, sched=sched, topo=topo, positions=[5, 9])
+        traces[mode] = tr
+        assert tr.steps == 2 and tr.estimated_time_s > 0
+        # event log: (time, actor, action, task) with reference actor names
+        acts = {}
+        for t_ns, actor, action, task in tr.event_log:
+            assert action in ("dispatch", "start", "complete")
+            assert actor.startswith("sched.x" if action == "dispatch" else "worker.x")
+            acts.setdefault((task, action), []).append(t_ns)
+        for t in g.tasks:
+            assert (t.id, "dispatch") in acts and (t.id, "complete") in acts, t.id
+            assert min(acts[(t.id, "start")]) >= min(acts[(t.id, "dispatch")]) - 2000
+            assert max(acts[(t.id, "complete")]) >= max(acts[(t.id, "start")])
+        j = tr.to_json()
+        assert list(j) == list(gold["traces"]["chiplet_b8"]["to_json"])
+        assert j["mode"] == mode and j["hbm_read_bytes"] > 0
+        row = tr.csv_row(f"{mode}_b2").split(",")
+        assert len(row) == len(report.CSV_COLUMNS) and row[1] == mode
+    table = report.comparison_table([(2, traces)])
+    assert "L2Hit% standard" in table and "HBMRd xstandard chiplet" in table
+    c = report.compare(traces["standard"], traces["chiplet"]).to_json()
+    assert c["baseline_mode"] == "standard" and c["ratios"]["dispatches"] > 0

@@ -205,3 +205,50 @@ def test_tensor_core_attention_lowering(fuse):
     for t in o_proj:
         assert low.event_names[t.wait0].endswith(want), low.event_names[t.wait0]
     assert ev  # events lowered
+
+
+def _ref_chipletsim():
+    import os
+    import sys
+    src = "/root/reference/pkg/src"
+    if not os.path.isdir(src):
+        pytest.skip("reference package not present (build container only)")
+    if src not in sys.path:
+        sys.path.insert(0, src)
+    return pytest.importorskip("chipletsim")
+
+
+@pytest.mark.parametrize("mode", ["chiplet", "standard"])
+@pytest.mark.parametrize("B", [1, 8])
+def test_lowers_a_graph_built_by_the_reference(mode, B):
+    """Drop-in boundary: a TaskGraph built by the REFERENCE's own
+    build_decoder_layer (chipletsim, ref taskgraph.py:355-526) lowers to
+    exactly the device descriptors of the same graph built here."""
+    import os
+
+    _ref_chipletsim()
+    from chipletsim import machine as rm
+    from chipletsim import taskgraph as rt
+    gold = os.path.join(os.path.dirname(__file__), "golden", "b200_machine.json")
+    m, mach = model_preset("toy"), preset("b200")
+    tiles = device_tiles(m, mach, mode, B)
+    rtiles = {(k if k == "silu_chunk" else rt.OpKind(k.value)): v for k, v in tiles.items()}
+    g_ref = rt.build_decoder_layer(rm.model_preset("toy"), rm.load_machine(gold), mode, B,
+                                   tile_overrides=rtiles, layers=2)
+    g_own = build_decoder_layer(m, mach, mode, B, tile_overrides=tiles, layers=2)
+    spec = Qwen3Spec.toy(layers=2)
+    w = Qwen3Weights.random(spec, seed=1)
+    lm = _default_lm_tile(spec, B)
+    per_die = mode == "chiplet"
+    slots = 2 * W if per_die else spec.vocab // lm[1]
+    opts = LoweringOptions(sched_mode=L.SCHED_PER_DIE if per_die else L.SCHED_FLAT,
+                           workers=W if per_die else 147, n_dies=2, fanout=True, lm_tile=lm)
+    lows = []
+    for g in (g_ref, g_own):
+        st = build_state(g, w, 128, lm, slots, device="cpu")
+        lows.append(lower(g, spec, st, opts))
+    a, b = lows
+    assert a.task_names == b.task_names and a.event_names == b.event_names
+    assert list(a.event_required) == list(b.event_required)
+    assert bytes(a.tasks) == bytes(b.tasks) and bytes(a.units) == bytes(b.units)
+    assert list(a.sched_begin) == list(b.sched_begin)
