@@ -35,6 +35,7 @@
 #ifndef MK_H
 #define MK_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -60,11 +61,21 @@ extern "C" {
 #define MK_OP_ATTN_REDUCE 4  /* OpKind.ATTN_REDUCE: merge split partials     */
 #define MK_OP_SILU 5         /* OpKind.SILU (standard mode only)             */
 #define MK_OP_ARGMAX 6       /* appended: greedy token from LM-head partials */
+#define MK_OP_TP_ALLREDUCE 7 /* tensor parallel: flags + rank-ordered sum of the
+                                fp32 partials every rank pushed into this rank's
+                                exchange region, + residual -> bf16 (not in the
+                                reference: SURVEY.md 8(e))  */
+#define MK_OP_TP_ARGMAX 8    /* tensor parallel: (max, index) of the local vocab
+                                shard pushed to every rank, global greedy token */
 
 #define MK_EPI_NONE 0
 #define MK_EPI_RESIDUAL 1 /* o_proj / down: y = x W^T + residual            */
 #define MK_EPI_SILU 2     /* fused gate/up halves: y = silu(g) * u           */
 #define MK_EPI_LOGITS 3   /* LM head: fp32 logits + per-worker argmax        */
+#define MK_EPI_PARTIAL 4  /* TP row-parallel o_proj / down: the fp32 partial
+                             product is stored straight into every rank's
+                             exchange region (y = byte offset of this rank's
+                             slot, identical on all ranks)                   */
 
 #define MK_BODY_GEMV 0   /* CUDA cores, 128-bit weight streaming (batch <= 16)  */
 #define MK_BODY_UMMA 1   /* tcgen05.mma: 128 weight rows x batch, TMEM accum.   */
@@ -79,6 +90,7 @@ extern "C" {
 
 #define MK_MAX_SMS 256
 #define MK_MAX_DIES 8
+#define MK_MAX_TP 8        /* tensor-parallel ranks                              */
 
 typedef struct mk_topology {
   int32_t num_sms;
@@ -206,6 +218,23 @@ typedef struct mk_argmax_params {
   int32_t M, n_slots;
 } mk_argmax_params;
 
+/* MK_OP_TP_ALLREDUCE (units split the d/8 column chunks) and
+ * MK_OP_TP_ARGMAX (one unit, all rows).  Offsets are bytes into the
+ * exchange region, identical on every rank (mk_tp_init). */
+typedef struct mk_tp_params {
+  int64_t recv_off;    /* ALLREDUCE: fp32 [world][M][d] partials of this point  */
+  int64_t flag_off;    /* uint32 [world]: epoch each rank announced this point  */
+  int64_t gather_off;  /* ARGMAX: {float val, int32 idx} [world][M]              */
+  const void* res;     /* ALLREDUCE: bf16 residual [M][d]                       */
+  void* y;             /* ALLREDUCE: bf16 [M][d] = res + sum_rank partial       */
+  const float* amax_val;   /* ARGMAX: local LM-head shard slots [n_slots][M]    */
+  const int32_t* amax_idx;
+  int32_t* out_tokens;
+  int32_t* next_tokens;
+  int32_t* positions;
+  int32_t M, d, n_slots, vocab0;  /* vocab0: first global row of this shard  */
+} mk_tp_params;
+
 typedef struct mk_graph_desc {
   int32_t n_tasks;
   int32_t n_events;
@@ -294,6 +323,22 @@ int mk_set_prefetch(mk_handle* h, int slots);
 /* Diagnostics only: bit0 = consumers skip GEMM math, bit1 = no TMA copies,
  * bit2 = count wait cycles (mk_counters wait_*). */
 int mk_set_debug(mk_handle* h, int flags);
+/* Tensor parallelism: `peer_bases[q]` is rank q's
+ * exchange region as addressable from this device (peer-mapped /
+ * IPC-opened; peer_bases[rank] = own region).  Call before the first step. */
+int mk_tp_init(mk_handle* h, int rank, int world, void* const* peer_bases);
+/* Exchange regions: plain cudaMalloc (IPC-exportable), zero-filled. */
+int mk_tp_alloc(int device, size_t bytes, void** out);
+int mk_tp_free(void* ptr);
+/* CUDA IPC handle (64 bytes) of an mk_tp_alloc region / open a peer's. */
+int mk_ipc_export(void* ptr, uint8_t* handle64);
+int mk_ipc_import(int device, const uint8_t* handle64, void** out);
+int mk_ipc_close(void* ptr);
+/* Launch geometry override (before the first step): `ctas` CTAs (flat
+ * scheduler only: workers <= ctas - 1) and cooperative (1) or plain (0)
+ * launches -- several ranks of a TP group can then share one GPU, each on
+ * its own subset of SMs (single-GPU test of the device TP path). */
+int mk_set_grid(mk_handle* h, int ctas, int cooperative);
 int mk_destroy(mk_handle* h);
 const char* mk_last_error(void);
 int mk_version(void);

@@ -15,13 +15,14 @@ LIB_PATH = os.environ.get("MK_LIB_PATH") or os.path.join(_HERE, "libmk.so")
 
 MK_OK, MK_ERR_CONFIG, MK_ERR_DEADLOCK, MK_ERR_CUDA = 0, 2, 3, 4
 LEVEL_WAVEFRONT, LEVEL_CU, LEVEL_CHIPLET = 0, 1, 2
-OP_NOP, OP_RMSNORM, OP_GEMM, OP_ATTN_PARTIAL, OP_ATTN_REDUCE, OP_SILU, OP_ARGMAX = range(7)
-EPI_NONE, EPI_RESIDUAL, EPI_SILU, EPI_LOGITS = range(4)
+(OP_NOP, OP_RMSNORM, OP_GEMM, OP_ATTN_PARTIAL, OP_ATTN_REDUCE, OP_SILU, OP_ARGMAX,
+ OP_TP_ALLREDUCE, OP_TP_ARGMAX) = range(9)
+EPI_NONE, EPI_RESIDUAL, EPI_SILU, EPI_LOGITS, EPI_PARTIAL = range(5)
 BODY_GEMV, BODY_UMMA = 0, 1
 TRAV_N_MAJOR, TRAV_M_MAJOR = 0, 1
 DIST_M_TILE, DIST_M_SPLIT = 0, 1
 SCHED_PER_DIE, SCHED_FLAT = 0, 1
-MAX_SMS, MAX_DIES = 256, 8
+MAX_SMS, MAX_DIES, MAX_TP = 256, 8, 8
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -84,6 +85,13 @@ class ArgmaxParams(C.Structure):
                 ("next_tokens", P), ("positions", P), ("M", I32), ("n_slots", I32)]
 
 
+class TPParams(C.Structure):
+    _fields_ = [("recv_off", C.c_int64), ("flag_off", C.c_int64), ("gather_off", C.c_int64),
+                ("res", P), ("y", P), ("amax_val", P), ("amax_idx", P),
+                ("out_tokens", P), ("next_tokens", P), ("positions", P),
+                ("M", I32), ("d", I32), ("n_slots", I32), ("vocab0", I32)]
+
+
 class GraphDesc(C.Structure):
     _fields_ = [("n_tasks", I32), ("n_events", I32), ("n_units", I32),
                 ("n_sub_ctrs", I32), ("n_schedulers", I32), ("sched_mode", I32),
@@ -114,6 +122,8 @@ EXPORTS = ("mk_probe", "mk_probe_raw", "mk_create", "mk_step", "mk_sync", "mk_co
            "mk_counters_reset", "mk_log_enable", "mk_log_read",
            "mk_tile_log_enable", "mk_tile_log_read", "mk_trace_enable", "mk_trace_read",
            "mk_set_watchdog", "mk_set_prefetch", "mk_set_debug",
+           "mk_tp_init", "mk_tp_alloc", "mk_tp_free", "mk_ipc_export", "mk_ipc_import",
+           "mk_ipc_close", "mk_set_grid",
            "mk_destroy", "mk_last_error", "mk_version")
 
 _lib = None
@@ -148,6 +158,13 @@ def load() -> C.CDLL:
     lib.mk_trace_read.restype = C.c_int64
     lib.mk_set_watchdog.argtypes = [C.c_void_p, C.c_double]
     lib.mk_set_debug.argtypes = [C.c_void_p, C.c_int]
+    lib.mk_tp_init.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+    lib.mk_tp_alloc.argtypes = [C.c_int, C.c_size_t, C.POINTER(C.c_void_p)]
+    lib.mk_tp_free.argtypes = [C.c_void_p]
+    lib.mk_ipc_export.argtypes = [C.c_void_p, C.POINTER(C.c_uint8)]
+    lib.mk_ipc_import.argtypes = [C.c_int, C.POINTER(C.c_uint8), C.POINTER(C.c_void_p)]
+    lib.mk_ipc_close.argtypes = [C.c_void_p]
+    lib.mk_set_grid.argtypes = [C.c_void_p, C.c_int, C.c_int]
     lib.mk_destroy.argtypes = [C.c_void_p]
     lib.mk_last_error.restype = C.c_char_p
     _lib = lib

@@ -57,6 +57,15 @@ def linear_gemm_dims(op: OpKind, model: ModelConfig) -> tuple:
     return table[op]
 
 
+def shard_gemm_dims(op: OpKind, model: ModelConfig, tp: int = 1) -> tuple:
+    """(K, N) of one tensor-parallel rank's shard of a linear op: QKV and
+    gate/up column-parallel (N / tp), O and down row-parallel (K / tp)."""
+    k, n = linear_gemm_dims(op, model)
+    if op in (OpKind.QKV_PROJ, OpKind.GATE_UP_SILU):
+        return k, n // tp
+    return k // tp, n
+
+
 def fit_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
               base: dict | None = None) -> dict:
     """Halve T_N / T_K until they divide the model's GEMMs (ref scenario.py:83-106).
@@ -113,10 +122,12 @@ def umma_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
 
 
 def device_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
-                 batch: int = 1, t_m: int | None = None, umma: bool | None = None) -> dict:
+                 batch: int = 1, t_m: int | None = None, umma: bool | None = None,
+                 tp: int = 1) -> dict:
     """Tile overrides for the device GEMM bodies: the tcgen05 body from
     UMMA_MIN_BATCH rows per m-tile on (when every per-task width divides its
-    128-row tiles), the CUDA-core warp-row GEMV below (see gemv_tiles)."""
+    128-row tiles), the CUDA-core warp-row GEMV below (see gemv_tiles).
+    ``tp``: tiles of one tensor-parallel rank's shard (shard_gemm_dims)."""
     if t_m is None:
         t_m = default_t_m(batch)
     use = umma if umma is not None else min(batch, t_m) >= UMMA_MIN_BATCH
@@ -124,7 +135,7 @@ def device_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
         tiles = umma_tiles(model, machine, graph_mode, t_m)
         ok = True
         for op in LINEAR_OPS:
-            k, n = linear_gemm_dims(op, model)
+            k, n = shard_gemm_dims(op, model, tp)
             width = n if graph_mode == "standard" else n // machine.num_xcds
             rows = 128 if not (op is OpKind.GATE_UP_SILU and graph_mode == "chiplet") else 128
             if op is OpKind.GATE_UP_SILU and graph_mode == "chiplet":
@@ -133,11 +144,11 @@ def device_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
             ok = ok and width % rows == 0 and k % 64 == 0
         if ok:
             return tiles
-    return gemv_tiles(model, machine, graph_mode, batch, min(t_m, 16))
+    return gemv_tiles(model, machine, graph_mode, batch, min(t_m, 16), tp)
 
 
 def gemv_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
-               batch: int = 1, t_m: int = 16) -> dict:
+               batch: int = 1, t_m: int = 16, tp: int = 1) -> dict:
     """B200 tile overrides for the warp-row GEMM body (csrc gemm_tile).
 
     One shared-memory ring slot holds ``R x T_K`` bf16 (16 KiB) with
@@ -153,7 +164,7 @@ def gemv_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
     r_fused = 16 if rows <= 4 else 32
     out = {}
     for op in LINEAR_OPS:
-        k, n = linear_gemm_dims(op, model)
+        k, n = shard_gemm_dims(op, model, tp)
         fused = op is OpKind.GATE_UP_SILU and graph_mode == "chiplet"
         width = n if graph_mode == "standard" else n // machine.num_xcds
         if fused:
@@ -169,7 +180,7 @@ def gemv_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
         while k % tk:
             tk //= 2
         out[op] = (t_m, tn, tk)
-    out["silu_chunk"] = min(STANDARD_TILE_PROFILE["silu_chunk"], model.ffn_dim)
+    out["silu_chunk"] = min(STANDARD_TILE_PROFILE["silu_chunk"], model.ffn_dim // tp)
     return out
 
 

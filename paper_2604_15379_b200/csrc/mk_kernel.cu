@@ -140,6 +140,10 @@ struct KArgs {
   int n_rows;
   uint64_t* trace;         // per-unit phase stamps [worker][trace_cap][8] (mk_trace_enable)
   int trace_cap;
+  // tensor parallelism (mk_tp_init): exchange region of every rank as
+  // addressable from this device; tp_peer[tp_rank] is this rank's own
+  int tp_world, tp_rank;
+  uint8_t* tp_peer[MK_MAX_TP];
 };
 
 struct AttnScratch {
@@ -318,6 +322,18 @@ __device__ __forceinline__ const T* P(const KArgs& a, const mk_task& t) {
   const Smem& s = *reinterpret_cast<const Smem*>(smem_raw);
   (void)a;
   return reinterpret_cast<const T*>(s.pcache[&t - s.tcache]);
+}
+
+// MK_EPI_PARTIAL: one fp32 partial-product element pushed into every rank's
+// exchange region (this rank's slot: byte offset p.y, row-major [M][ldy]).
+// Remote stores are posted over NVLink; the unit fences at system scope
+// before it signals (tp_partial_done), so the TP_ALLREDUCE announcement that
+// follows the local event orders them for the peers.
+__device__ __forceinline__ void tp_store(const KArgs& a, const mk_gemm_params& p, int row, int col,
+                                         float v) {
+  const size_t off = reinterpret_cast<size_t>(p.y) + (size_t(row) * p.ldy + col) * 4;
+  for (int q = 0; q < a.tp_world; ++q)
+    __stcg(reinterpret_cast<float*>(a.tp_peer[q] + off), v);
 }
 
 // ---------------------------------------------------------------------------
@@ -835,6 +851,12 @@ __device__ void gemm_tile(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
         if (v > amv[b] || (v == amv[b] && col < ami[b])) { amv[b] = v; ami[b] = col; }
       }
     } else {
+      if (p.epilogue == MK_EPI_PARTIAL) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < rpw) tp_store(a, p, m0 + b, out_col0 + warp + kConsWarps * j, acc[j][b]);
+        continue;
+      }
       uint16_t* y = reinterpret_cast<uint16_t*>(p.y) + size_t(m0 + b) * p.ldy;
       if (silu) {              // gate rows j < rpw/2, up rows j + rpw/2
 #pragma unroll
@@ -965,6 +987,9 @@ __device__ void gemm_tile_fast(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
         if (y) y[size_t(m0 + b) * p.ldy + col] = v;
         if (v > amv[b] || (v == amv[b] && col < ami[b])) { amv[b] = v; ami[b] = col; }
       }
+    } else if (p.epilogue == MK_EPI_PARTIAL) {
+#pragma unroll
+      for (int j = 0; j < RPW; ++j) tp_store(a, p, m0 + b, out_col0 + warp + kConsWarps * j, tot[j][b]);
     } else {
       uint16_t* y = reinterpret_cast<uint16_t*>(p.y) + size_t(m0 + b) * p.ldy;
       if (p.epilogue == MK_EPI_SILU) {
@@ -1099,6 +1124,9 @@ __device__ __forceinline__ void gemm_tile_fast_ks(const KArgs& a, Smem& s, uint8
         if (y) y[size_t(m0 + b) * p.ldy + col] = v;
         if (v > amv[b] || (v == amv[b] && col < ami[b])) { amv[b] = v; ami[b] = col; }
       }
+    } else if (p.epilogue == MK_EPI_PARTIAL) {
+#pragma unroll
+      for (int j = 0; j < RPW; ++j) tp_store(a, p, m0 + b, out_col0 + warp + kConsWarps * j, tot[j][b]);
     } else {
       uint16_t* y = reinterpret_cast<uint16_t*>(p.y) + size_t(m0 + b) * p.ldy;
       if (p.epilogue == MK_EPI_SILU) {
@@ -1492,7 +1520,7 @@ __device__ __forceinline__ void umma_res16(const mk_gemm_params& p, int m0, int 
   }
 }
 
-__device__ __forceinline__ void umma_epi16(Smem& s, const mk_gemm_params& p, int m0, int rows_m,
+__device__ __forceinline__ void umma_epi16(const KArgs& a, Smem& s, const mk_gemm_params& p, int m0, int rows_m,
                                            int out_col0, int row, int q, int lane, int cw, int j,
                                            const float (&v)[16], const float* rpre = nullptr) {
   if (p.epilogue == MK_EPI_LOGITS) {
@@ -1517,6 +1545,11 @@ __device__ __forceinline__ void umma_epi16(Smem& s, const mk_gemm_params& p, int
         if (val > bv || (val == bv && idx < bx)) { bv = val; bx = idx; }
       }
     }
+  } else if (p.epilogue == MK_EPI_PARTIAL) {
+    const int col = out_col0 + row;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (16 * j + i < rows_m) tp_store(a, p, m0 + 16 * j + i, col, v[i]);
   } else if (p.epilogue == MK_EPI_SILU) {
     // rows 32q..32q+15 are gate rows 16q.., rows 32q+16.. the matching up rows
     uint16_t* y = reinterpret_cast<uint16_t*>(p.y);
@@ -1580,7 +1613,7 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
         float rv[16], v[16];
         umma_res16(p, m0, rows_m, out_col0 + row, j, rv);
         tmem_acc16(s.tmem_base, q, buf, j, v);
-        umma_epi16(s, p, m0, rows_m, out_col0, row, q, lane, cw, j, v, rv);
+        umma_epi16(a, s, p, m0, rows_m, out_col0, row, q, lane, cw, j, v, rv);
       }
       tc_fence_before();
       __syncwarp();
@@ -1649,7 +1682,7 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] += t[u][i];
       }
-      umma_epi16(s, p, m0, rows_m, out_col0, row, q, lane, cw, j, v, rv);
+      umma_epi16(a, s, p, m0, rows_m, out_col0, row, q, lane, cw, j, v, rv);
     }
     tc_fence_before();
     __syncwarp();
@@ -2645,6 +2678,110 @@ __device__ void run_argmax(const KArgs& a, Smem& s, const mk_task& t, int ib, in
 }
 
 // ---------------------------------------------------------------------------
+// Tensor parallelism: the per-layer allreduce of the
+// row-parallel o_proj / down partials and the vocab-parallel greedy token,
+// as device tasks over peer memory.  The GEMMs (MK_EPI_PARTIAL) already
+// pushed their fp32 partials into every rank's exchange region; these tasks
+// only exchange epoch flags (st.release.sys / ld.acquire.sys, monotone: no
+// reset between steps) and reduce LOCAL memory in rank order, so every rank
+// computes bit-identical sums.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t* tp_flag(const KArgs& a, int q, int64_t flag_off, int slot) {
+  return reinterpret_cast<uint32_t*>(a.tp_peer[q] + flag_off) + slot;
+}
+
+// ct 0: announce this rank at the point (to every rank), wait for all ranks
+__device__ bool tp_rendezvous(const KArgs& a, int64_t flag_off, bool announce) {
+  if (announce) {
+    fence_sc_sys();
+    for (int q = 0; q < a.tp_world; ++q) st_release_sys(tp_flag(a, q, flag_off, a.tp_rank), a.epoch);
+  }
+  for (int q = 0; q < a.tp_world; ++q) {
+    const uint32_t* f = tp_flag(a, a.tp_rank, flag_off, q);
+    Spin sp;
+    while ((int32_t)(ld_acquire_sys(f) - a.epoch) < 0)
+      if (!sp.ok(a, -19)) return false;
+  }
+  return true;
+}
+
+// units split the row's d/8 column chunks; items [ib, ie) of d/8
+__device__ void run_tp_allreduce(const KArgs& a, Smem& s, const mk_task& t, int ib, int ie, int ct) {
+  const mk_tp_params& p = *P<mk_tp_params>(a, t);
+  if (ct == 0) tp_rendezvous(a, p.flag_off, ib == 0);
+  bar_sync(1, kCons);
+  const float* recv = reinterpret_cast<const float*>(a.tp_peer[a.tp_rank] + p.recv_off);
+  const size_t plane = size_t(p.M) * p.d;
+  const int n = (ie - ib) * p.M;
+  for (int e = ct; e < n; e += kCons) {
+    const int b = e / (ie - ib), c = (ib + e % (ie - ib)) * 8;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int q = 0; q < a.tp_world; ++q) {         // rank order: identical on every rank
+      const float* src = recv + q * plane + size_t(b) * p.d + c;
+      const float4 u = __ldcg(reinterpret_cast<const float4*>(src));
+      const float4 w = __ldcg(reinterpret_cast<const float4*>(src + 4));
+      acc[0] += u.x; acc[1] += u.y; acc[2] += u.z; acc[3] += u.w;
+      acc[4] += w.x; acc[5] += w.y; acc[6] += w.z; acc[7] += w.w;
+    }
+    float r[8];
+    unpack8(ldg128_cg(reinterpret_cast<const uint16_t*>(p.res) + size_t(b) * p.d + c), r);
+    uint16_t o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = f2bf(acc[k] + r[k]);
+    *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.y) + size_t(b) * p.d + c) =
+        *reinterpret_cast<uint4*>(o);
+  }
+}
+
+// one unit: the local shard's best (max logit, lowest global index) per row
+// goes to every rank; every rank then picks the global best the same way
+__device__ void run_tp_argmax(const KArgs& a, Smem& s, const mk_task& t, int ct) {
+  const mk_tp_params& p = *P<mk_tp_params>(a, t);
+  const int warp = ct >> 5, lane = ct & 31;
+  for (int b = warp; b < p.M; b += kConsWarps) {
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int q = lane; q < p.n_slots; q += 32) {
+      const float v = __ldcg(p.amax_val + size_t(q) * p.M + b);
+      const int i = __ldcg(p.amax_idx + size_t(q) * p.M + b);
+      if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float v2 = __shfl_xor_sync(0xffffffffu, best, off);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (v2 > best || (v2 == best && i2 < bi)) { best = v2; bi = i2; }
+    }
+    if (lane == 0) {
+      const int gi = bi == 0x7fffffff ? bi : bi + p.vocab0;
+      for (int q = 0; q < a.tp_world; ++q) {
+        int32_t* g = reinterpret_cast<int32_t*>(a.tp_peer[q] + p.gather_off) + 2 * (size_t(a.tp_rank) * p.M + b);
+        __stcg(reinterpret_cast<float*>(g), best);
+        __stcg(g + 1, gi);
+      }
+    }
+  }
+  __syncwarp();
+  fence_sc_sys();                                  // every writer, before the announcement
+  bar_sync(1, kCons);
+  if (ct == 0) tp_rendezvous(a, p.flag_off, true);
+  bar_sync(1, kCons);
+  const int32_t* gat = reinterpret_cast<const int32_t*>(a.tp_peer[a.tp_rank] + p.gather_off);
+  for (int b = ct; b < p.M; b += kCons) {
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int q = 0; q < a.tp_world; ++q) {
+      const float v = __ldcg(reinterpret_cast<const float*>(gat + 2 * (size_t(q) * p.M + b)));
+      const int i = __ldcg(gat + 2 * (size_t(q) * p.M + b) + 1);
+      if (v > best || (v == best && i < bi)) { best = v; bi = i; }
+    }
+    p.out_tokens[b] = bi;
+    p.next_tokens[b] = bi;
+    p.positions[b] = p.positions[b] + 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Roles
 // ---------------------------------------------------------------------------
 __device__ void log_rec(const KArgs& a, int kind, int task, int ib, int worker, int die,
@@ -2959,9 +3096,13 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
       case MK_OP_ATTN_REDUCE: run_attn_reduce(a, s, t, ent.y, ent.z, ct); break;
       case MK_OP_SILU: run_silu(a, t, ct); break;
       case MK_OP_ARGMAX: run_argmax(a, s, t, ent.y, ent.z, ct); break;
+      case MK_OP_TP_ALLREDUCE: run_tp_allreduce(a, s, t, ent.y, ent.z, ct); break;
+      case MK_OP_TP_ARGMAX: run_tp_argmax(a, s, t, ct); break;
       default: break;
     }
     MK_TRACE(a, s, ct, 4);
+    if (t.op == MK_OP_GEMM && a.tp_world > 1 && P<mk_gemm_params>(a, t)->epilogue == MK_EPI_PARTIAL)
+      fence_sc_sys();                   // pushed partials performed before the local signal
     bar_sync(1, kCons);
     if (ct == 0) {
       if (a.trace) s.tr[5] = globaltimer();
@@ -3210,6 +3351,10 @@ struct mk_handle {
   unsigned long long* d_tile_cursor = nullptr;
   long long tile_cap = 0;
   std::vector<int32_t> group_size;
+  int cooperative = 1;
+  int tp_world = 1, tp_rank = 0;
+  uint8_t* tp_peer[MK_MAX_TP] = {};
+  bool has_tp_tasks = false;
 };
 
 static const void* kernel_for(int feat) {
@@ -3435,6 +3580,17 @@ static int validate_graph(const mk_graph_desc* g) {
         return fail(MK_ERR_CONFIG, "attention task " + std::to_string(i) + " has unsupported shapes");
     }
   }
+  for (int i = 0; i < g->n_tasks; ++i) {
+    const mk_task& t = g->tasks[i];
+    if (t.op == MK_OP_TP_ALLREDUCE || t.op == MK_OP_TP_ARGMAX) {
+      const mk_tp_params* p = reinterpret_cast<const mk_tp_params*>(
+          static_cast<const uint8_t*>(g->params) + t.param_off);
+      if (t.level == MK_LEVEL_CHIPLET || p->flag_off < 0 || p->flag_off % 4 ||
+          (t.op == MK_OP_TP_ALLREDUCE && (p->d % 8 || p->recv_off % 16 || !p->res || !p->y)) ||
+          (t.op == MK_OP_TP_ARGMAX && (t.n_units != 1 || p->gather_off % 8)))
+        return fail(MK_ERR_CONFIG, "tensor-parallel task " + std::to_string(i) + " has a bad setup");
+    }
+  }
   for (int u = 0; u < g->n_units; ++u)
     if (g->units[u].task < 0 || g->units[u].task >= g->n_tasks)
       return fail(MK_ERR_CONFIG, "unit " + std::to_string(u) + " references an unknown task");
@@ -3605,6 +3761,8 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
     }
     if (lean && !(n_umma && n_gemv)) h->feat |= kFeatLean;
   }
+  for (int i = 0; i < g->n_tasks; ++i)
+    if (g->tasks[i].op == MK_OP_TP_ALLREDUCE || g->tasks[i].op == MK_OP_TP_ARGMAX) h->has_tp_tasks = true;
   h->kernel = kernel_for(h->feat);
   CK(cudaFuncSetAttribute(h->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmemBytes)));
   int occ = 0;
@@ -3653,9 +3811,18 @@ int mk_step(mk_handle* h, void* stream) {
   a.trace = h->trace_cap ? h->d_trace : nullptr;
   a.positions = h->positions; a.n_rows = h->n_rows;
   a.trace_cap = h->trace_cap;
+  a.tp_world = h->tp_world; a.tp_rank = h->tp_rank;
+  for (int q = 0; q < MK_MAX_TP; ++q) a.tp_peer[q] = h->tp_peer[q];
+  if (h->has_tp_tasks && h->tp_world < 2)
+    return fail(MK_ERR_CONFIG, "graph has tensor-parallel tasks: call mk_tp_init first");
   void* args[] = {&a};
-  CK(cudaLaunchCooperativeKernel(h->kernel, dim3(h->num_sms), dim3(kThreads), args,
-                                 kSmemBytes, static_cast<cudaStream_t>(stream)));
+  if (h->cooperative) {
+    CK(cudaLaunchCooperativeKernel(h->kernel, dim3(h->num_sms), dim3(kThreads), args,
+                                   kSmemBytes, static_cast<cudaStream_t>(stream)));
+  } else {
+    CK(cudaLaunchKernel(h->kernel, dim3(h->num_sms), dim3(kThreads), args,
+                        kSmemBytes, static_cast<cudaStream_t>(stream)));
+  }
   h->epoch = a.epoch;
   return MK_OK;
 }
@@ -3787,6 +3954,68 @@ int mk_set_prefetch(mk_handle* h, int slots) {
 int mk_set_debug(mk_handle* h, int flags) {
   if (!h) return fail(MK_ERR_CONFIG, "null handle");
   h->debug = flags;
+  return MK_OK;
+}
+
+int mk_tp_init(mk_handle* h, int rank, int world, void* const* peer_bases) {
+  if (!h) return fail(MK_ERR_CONFIG, "null handle");
+  if (world < 1 || world > MK_MAX_TP || rank < 0 || rank >= world || (world > 1 && !peer_bases))
+    return fail(MK_ERR_CONFIG, "bad tensor-parallel rank / world / peers");
+  if (h->epoch != 0) return fail(MK_ERR_CONFIG, "mk_tp_init after the first step");
+  for (int q = 0; q < world; ++q)
+    if (!peer_bases[q]) return fail(MK_ERR_CONFIG, "null peer exchange region");
+  h->tp_rank = rank;
+  h->tp_world = world;
+  for (int q = 0; q < MK_MAX_TP; ++q)
+    h->tp_peer[q] = q < world ? static_cast<uint8_t*>(peer_bases[q]) : nullptr;
+  return MK_OK;
+}
+
+int mk_tp_alloc(int device, size_t bytes, void** out) {
+  if (!out || bytes == 0) return fail(MK_ERR_CONFIG, "bad exchange-region request");
+  CK(cudaSetDevice(device));
+  CK(cudaMalloc(out, bytes));
+  CK(cudaMemset(*out, 0, bytes));
+  return MK_OK;
+}
+
+int mk_tp_free(void* ptr) {
+  if (ptr) CK(cudaFree(ptr));
+  return MK_OK;
+}
+
+int mk_ipc_export(void* ptr, uint8_t* handle64) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  cudaIpcMemHandle_t hd;
+  CK(cudaIpcGetMemHandle(&hd, ptr));
+  std::memcpy(handle64, &hd, sizeof(hd));
+  return MK_OK;
+}
+
+int mk_ipc_import(int device, const uint8_t* handle64, void** out) {
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle64, sizeof(hd));
+  CK(cudaSetDevice(device));
+  CK(cudaIpcOpenMemHandle(out, hd, cudaIpcMemLazyEnablePeerAccess));
+  return MK_OK;
+}
+
+int mk_ipc_close(void* ptr) {
+  if (ptr) CK(cudaIpcCloseMemHandle(ptr));
+  return MK_OK;
+}
+
+int mk_set_grid(mk_handle* h, int ctas, int cooperative) {
+  if (!h) return fail(MK_ERR_CONFIG, "null handle");
+  if (h->epoch != 0) return fail(MK_ERR_CONFIG, "mk_set_grid after the first step");
+  if (h->sched_mode != MK_SCHED_FLAT || ctas < 2 || ctas > h->num_sms || h->W > ctas - 1)
+    return fail(MK_ERR_CONFIG, "mk_set_grid: flat scheduler, 2..#SMs CTAs, workers <= ctas - 1");
+  CK(cudaSetDevice(h->device));
+  h->num_sms = ctas;
+  h->group_size[0] = ctas;
+  CK(cudaMemcpy(h->d_group_size, h->group_size.data(), sizeof(int32_t) * MK_MAX_DIES,
+                cudaMemcpyHostToDevice));
+  h->cooperative = cooperative ? 1 : 0;
   return MK_OK;
 }
 

@@ -22,6 +22,18 @@ __device__ __forceinline__ uint64_t globaltimer() {
 }
 
 // ---- gpu-scope synchronisation (event counters, mailboxes) -------------
+// system scope (peer GPUs over NVLink): tensor-parallel exchange flags
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_sc_sys() {
+  asm volatile("fence.sc.sys;" ::: "memory");
+}
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -85,6 +85,70 @@ def tp_plan(spec, tp: int, rank: int) -> TPPlan:
                   range(rank * v, (rank + 1) * v), spec.hidden)
 
 
+def shard_spec(spec, tp: int):
+    """The Qwen3Spec of one rank's shard (hidden / head_dim replicated)."""
+    from dataclasses import replace
+    plan = tp_plan(spec, tp, 0)
+    return replace(spec, ffn=len(plan.ffn), q_heads=len(plan.q_heads),
+                   kv_heads=len(plan.kv_heads), vocab=len(plan.vocab))
+
+
+def shard_weights(w, tp: int, rank: int):
+    """Rank ``rank``'s slices of the canonical weights (tp_plan): QKV rows of
+    its kv-head groups, O columns of its q heads, gate/up rows and down
+    columns of its FFN range, LM-head rows of its vocab range; embedding and
+    norm gammas replicated."""
+    from .weights import Qwen3Weights
+    sp = w.spec
+    plan = tp_plan(sp, tp, rank)
+    hd = sp.head_dim
+    qs = slice(plan.q_heads.start * hd, plan.q_heads.stop * hd)
+    ks = slice(plan.kv_heads.start * hd, plan.kv_heads.stop * hd)
+    fs = slice(plan.ffn.start, plan.ffn.stop)
+    layers = []
+    for L in w.layers:
+        layers.append({"q": L["q"][qs].contiguous(), "k": L["k"][ks].contiguous(),
+                       "v": L["v"][ks].contiguous(), "o": L["o"][:, qs].contiguous(),
+                       "gate": L["gate"][fs].contiguous(), "up": L["up"][fs].contiguous(),
+                       "down": L["down"][:, fs].contiguous(),
+                       **{k: L[k] for k in ("q_norm", "k_norm", "in_norm", "post_norm")}})
+    return Qwen3Weights(shard_spec(sp, tp), w.embed, w.final_norm,
+                        w.lm_head[plan.vocab.start:plan.vocab.stop].contiguous(), layers)
+
+
+def connect_local(mks):
+    """Join the Megakernels of one TP group living in this process (same
+    GPU, or GPUs with peer access): every rank gets every rank's exchange
+    region pointer (mk_tp_init)."""
+    bases = [mk.tp_region for mk in mks]
+    for mk in mks:
+        mk.tp_connect(bases)
+
+
+def connect_dist(mk):
+    """Join a TP group of one process per GPU (torch.distributed over
+    NCCL/gloo for the bootstrap only): CUDA IPC handles of the exchange
+    regions are all-gathered, each peer's region opened, mk_tp_init."""
+    import ctypes as C
+    from . import _lib as L
+    lib = L.load()
+    h = (C.c_uint8 * 64)()
+    L.check(lib.mk_ipc_export(C.c_void_p(mk.tp_region), h))
+    handles = [None] * dist.get_world_size()
+    dist.all_gather_object(handles, bytes(h))
+    bases = []
+    for q, hb in enumerate(handles):
+        if q == mk.tp[0]:
+            bases.append(mk.tp_region)
+            continue
+        buf = (C.c_uint8 * 64).from_buffer_copy(hb)
+        ptr = C.c_void_p()
+        L.check(lib.mk_ipc_import(mk.device, buf, C.byref(ptr)))
+        mk.tp_opened.append(ptr.value)
+        bases.append(ptr.value)
+    mk.tp_connect(bases)
+
+
 def allreduce_bytes_per_step(spec, batch: int, dtype_bytes: int = 2) -> dict:
     """Two row-parallel allreduces of [B, hidden] per layer."""
     per = batch * spec.hidden * dtype_bytes

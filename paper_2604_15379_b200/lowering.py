@@ -89,6 +89,47 @@ class LoweringOptions:
                                    # measured slower (one warp merges serially)
     ksplit: bool = True            # die tasks: K-split slot ranges per worker
                                    # instead of whole tiles
+    tp_rank: int = 0               # tensor parallelism: this
+    tp_world: int = 1              # rank of the group; spec / buffers are the
+    tp_layout: object = None       # rank's shard (runtime.build_state), TPLayout
+
+
+@dataclass(frozen=True)
+class TPLayout:
+    """Byte layout of one rank's exchange region -- identical on every rank,
+    so the offsets baked into the descriptors address any rank's region:
+    recv[point][world][B][d] fp32 (point 2l = layer l's o_proj, 2l+1 its
+    down proj; slot q = rank q's partial), flags[point][world] uint32
+    (point 2L = the LM-head argmax), gather[world][B] {float, int32}."""
+    world: int
+    batch: int
+    hidden: int
+    layers: int
+
+    @property
+    def n_points(self) -> int:
+        return 2 * self.layers
+
+    def recv_off(self, point: int) -> int:
+        return point * self.world * self.batch * self.hidden * 4
+
+    def slot_off(self, point: int, rank: int) -> int:
+        return self.recv_off(point) + rank * self.batch * self.hidden * 4
+
+    def flag_off(self, point: int) -> int:
+        return self.recv_off(self.n_points) + point * self.world * 4
+
+    @property
+    def argmax_point(self) -> int:
+        return self.n_points
+
+    @property
+    def gather_off(self) -> int:
+        return -(-self.flag_off(self.n_points + 1) // 16) * 16
+
+    @property
+    def nbytes(self) -> int:
+        return self.gather_off + self.world * self.batch * 8
 
 XS_BYTES = 32768                   # kXsBytes in mk_kernel.cu
 PIECE_FLOATS = 128 * 64            # K-split piece: 128 weight rows x 64 batch rows
@@ -148,9 +189,15 @@ class _Blob:
         return off
 
 
+class _Off(int):
+    """A byte offset standing in for a pointer (MK_EPI_PARTIAL's y)."""
+
+
 def _ptr(t, elem_offset=0):
     if t is None:
         return None
+    if isinstance(t, _Off):
+        return int(t) + elem_offset * 4
     return t.data_ptr() + elem_offset * t.element_size()
 
 
@@ -321,6 +368,33 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
     # would only add a completion hop to the critical path
     bypass = {}
 
+    tp = opts.tp_world > 1
+    if tp and (opts.tp_layout is None or opts.tp_layout.world != opts.tp_world):
+        raise ValueError("tensor-parallel lowering needs the group's TPLayout")
+    kv0 = opts.tp_rank * spec.kv_heads              # first kv head of this rank's shard
+    # the last task of every (layer, row-parallel op): its allreduce follows it
+    last_of = {}
+    for gi, t in enumerate(g.tasks):
+        if t.op_kind in (OpKind.O_PROJ_RESIDUAL, OpKind.DOWN_PROJ_RESIDUAL):
+            last_of[(t.id.split(".")[0], t.op_kind)] = gi
+    u_ar = max(1, min(total_workers, d // 8 // 32))
+
+    def add_allreduce(layer, kind, wait, res, y):
+        point = 2 * layer + (0 if kind is OpKind.O_PROJ_RESIDUAL else 1)
+        ev = f"e.L{layer}.{'o' if point % 2 == 0 else 'down'}_allreduce"
+        ev_index[ev] = len(event_names)
+        event_names.append(ev)
+        required.append(1)
+        p = L.TPParams()
+        p.recv_off = opts.tp_layout.recv_off(point)
+        p.flag_off = opts.tp_layout.flag_off(point)
+        p.res, p.y = _ptr(res), _ptr(y)
+        p.M, p.d = B, d
+        add_task(f"L{layer}.{'o' if point % 2 == 0 else 'down'}_allreduce.t0", -1,
+                 L.OP_TP_ALLREDUCE, L.LEVEL_CU, None, wait, ev, blob.add(p), layer,
+                 n_items=d // 8, n_units=u_ar)
+        bypass[wait] = ev            # consumers of the partial GEMM wait on the sum
+
     for gi, t in enumerate(g.tasks):
         layer = int(t.id.split(".")[0][1:])
         lb = bufs.layers[layer]
@@ -345,7 +419,14 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                 bypass[t.signal_event] = wait
         elif op in (OpKind.QKV_PROJ, OpKind.O_PROJ_RESIDUAL,
                     OpKind.GATE_UP_SILU, OpKind.DOWN_PROJ_RESIDUAL):
-            M, K, N = t.gemm_shape
+            # this rank's shard of the device-wide GEMM (== the graph's
+            # gemm_shape without tensor parallelism)
+            M, K, N = {OpKind.QKV_PROJ: (B, d, spec.qkv_dim),
+                       OpKind.O_PROJ_RESIDUAL: (B, spec.q_heads * hd, d),
+                       OpKind.GATE_UP_SILU: (B, d, 2 * F),
+                       OpKind.DOWN_PROJ_RESIDUAL: (B, F, d)}[op]
+            if not tp:
+                assert (M, K, N) == tuple(t.gemm_shape), (t.id, (M, K, N), t.gemm_shape)
             tile = tuple(t.tile_shape)
             x_in = bufs.x_in0 if layer == 0 else bufs.layers[layer - 1]["x_out"]
             gamma = None
@@ -358,7 +439,7 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
             elif op is OpKind.O_PROJ_RESIDUAL:
                 w, x, y, res, epi, ldx, ldy = (bufs.w_packed[layer]["o"],
                                               lb["attn_out"], lb["x_mid"], x_in,
-                                              L.EPI_RESIDUAL, d, d)
+                                              L.EPI_RESIDUAL, K, d)
             elif op is OpKind.GATE_UP_SILU:
                 fused = t.level is TaskLevel.CHIPLET
                 w = bufs.w_packed[layer]["gate_up"]
@@ -374,6 +455,14 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                 w, x, y, res, epi, ldx, ldy = (bufs.w_packed[layer]["down"],
                                               lb["silu_out"], lb["x_out"],
                                               lb["x_mid"], L.EPI_RESIDUAL, F, d)
+            ar = None
+            if tp and op in (OpKind.O_PROJ_RESIDUAL, OpKind.DOWN_PROJ_RESIDUAL):
+                # row-parallel: the fp32 partial goes to every rank (y is this
+                # rank's slot offset in the exchange regions), residual later
+                ar = (res, y)
+                point = 2 * layer + (0 if op is OpKind.O_PROJ_RESIDUAL else 1)
+                y = _Off(opts.tp_layout.slot_off(point, opts.tp_rank))
+                res, epi = None, L.EPI_PARTIAL
             if t.level is TaskLevel.CHIPLET:
                 X = g.machine.num_xcds
                 n_loc = N // X
@@ -391,14 +480,25 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                                  tm=work.m_idx, tn=work.n_idx, gamma=gamma)
                 add_task(t.id, gi, L.OP_GEMM, level, None, wait, t.signal_event,
                          po, layer)
+            if ar is not None and gi == last_of[(t.id.split(".")[0], op)]:
+                add_allreduce(layer, op, t.signal_event, *ar)
         elif op is OpKind.ATTN_PARTIAL:
-            h = int(t.id.rsplit(".t", 1)[1])
-            po = attn_params(layer, h, out=lb["attn_out"], fuse=True)
+            # tensor parallel: kv heads outside this rank's shard keep their
+            # task (the graph topology is unchanged) with no items
+            h = int(t.id.rsplit(".t", 1)[1]) - kv0
+            mine = 0 <= h < spec.kv_heads
+            po = attn_params(layer, h if mine else 0, out=lb["attn_out"], fuse=True)
             add_task(t.id, gi, L.OP_ATTN_PARTIAL, level, None, wait,
-                     t.signal_event, po, layer, n_items=B * bufs.n_splits,
+                     t.signal_event, po, layer, n_items=B * bufs.n_splits if mine else 0,
                      n_units=u_attn)
         elif op is OpKind.ATTN_REDUCE:
-            h = int(t.id.rsplit(".t", 1)[1])
+            h = int(t.id.rsplit(".t", 1)[1]) - kv0
+            mine = 0 <= h < spec.kv_heads
+            if not mine:
+                po = attn_params(layer, 0, out=lb["attn_out"], reduce_noop=fused_reduce)
+                add_task(t.id, gi, L.OP_ATTN_REDUCE, level, None, wait,
+                         t.signal_event, po, layer, n_items=0, n_units=1)
+                continue
             po = attn_params(layer, h, out=lb["attn_out"], reduce_noop=fused_reduce)
             if fused_reduce:
                 # merged inside ATTN_PARTIAL: the task stays in the graph as a
@@ -418,7 +518,7 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
             raise ValueError(f"cannot lower {op}")
 
     # ---- appended stages: final norm -> LM head -> argmax ---------------
-    last_event = g.tasks[-1].signal_event
+    last_event = bypass.get(g.tasks[-1].signal_event, g.tasks[-1].signal_event)
     n_layers = len(bufs.layers)
     for e in ("e.final_norm", "e.lm_head", "e.argmax"):
         ev_index[e] = len(event_names)
@@ -461,13 +561,26 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                          None, lm_wait, "e.lm_head", po, n_layers)
         required[ev_index["e.lm_head"]] = mt * nt
         amax_slots = nt
-    p = L.ArgmaxParams()
-    p.amax_val, p.amax_idx = _ptr(bufs.amax_val), _ptr(bufs.amax_idx)
-    p.out_tokens, p.next_tokens = _ptr(bufs.out_tokens), _ptr(bufs.tokens)
-    p.positions = _ptr(bufs.positions)
-    p.M, p.n_slots = B, amax_slots
-    add_task("argmax.t0", -1, L.OP_ARGMAX, L.LEVEL_CU, None, "e.lm_head",
-             "e.argmax", blob.add(p), n_layers, n_items=B, n_units=u_rows)
+    if tp:
+        # vocab-parallel LM head: (max, global index) of the shard to every
+        # rank, the same global pick on each (lowest index on ties)
+        p = L.TPParams()
+        p.flag_off = opts.tp_layout.flag_off(opts.tp_layout.argmax_point)
+        p.gather_off = opts.tp_layout.gather_off
+        p.amax_val, p.amax_idx = _ptr(bufs.amax_val), _ptr(bufs.amax_idx)
+        p.out_tokens, p.next_tokens = _ptr(bufs.out_tokens), _ptr(bufs.tokens)
+        p.positions = _ptr(bufs.positions)
+        p.M, p.d, p.n_slots, p.vocab0 = B, d, amax_slots, opts.tp_rank * spec.vocab
+        add_task("argmax.t0", -1, L.OP_TP_ARGMAX, L.LEVEL_CU, None, "e.lm_head",
+                 "e.argmax", blob.add(p), n_layers, n_items=B, n_units=1)
+    else:
+        p = L.ArgmaxParams()
+        p.amax_val, p.amax_idx = _ptr(bufs.amax_val), _ptr(bufs.amax_idx)
+        p.out_tokens, p.next_tokens = _ptr(bufs.out_tokens), _ptr(bufs.tokens)
+        p.positions = _ptr(bufs.positions)
+        p.M, p.n_slots = B, amax_slots
+        add_task("argmax.t0", -1, L.OP_ARGMAX, L.LEVEL_CU, None, "e.lm_head",
+                 "e.argmax", blob.add(p), n_layers, n_items=B, n_units=u_rows)
     required[ev_index["e.argmax"]] = 1
 
     flat_units = [u for s in units_by_sched for u in s]

@@ -207,23 +207,38 @@ class Megakernel:
                  sched: str = "per_die", topo: L.Topology | None = None,
                  fanout: bool = True, lm_tile=None, device: int = 0,
                  keep_logits: bool = True, watchdog_s: float = 10.0,
-                 ksplit: bool = True, fuse_attn_reduce: bool = False):
+                 ksplit: bool = True, fuse_attn_reduce: bool = False,
+                 tp: tuple | None = None, ctas: int | None = None,
+                 cooperative: bool = True):
+        """``tp=(rank, world)``: this rank's shard of a Megatron tensor-
+        parallel group (``weights`` are the full model; dist.shard_weights
+        slices them); join the group with dist.connect_local /
+        dist.connect_dist before the first step.  ``ctas`` (flat scheduler
+        only) launches that many CTAs -- several ranks can then share one GPU
+        on disjoint SMs (``cooperative=False``: plain launches)."""
         if not torch.cuda.is_available():
             raise RuntimeError("Megakernel needs a CUDA device (no CPU fallback)")
         self.lib = L.load()
         torch.cuda.set_device(device)
         self.device = device
         self.graph = g = adopt_graph(g)
+        self.tp = tuple(tp) if tp else (0, 1)
+        self.tp_region, self.tp_opened = None, []
+        if self.tp[1] > 1:
+            from .dist import shard_weights
+            weights = shard_weights(weights, self.tp[1], self.tp[0])
         self.spec = weights.spec
         if topo is None:
             topo = probe(device)
         self.topo = topo
         per_die = sched == "per_die"
+        if ctas is not None and per_die:
+            raise ValueError("ctas: flat scheduler only")
         if per_die:
             workers = g.machine.workers_per_xcd
             n_dies = g.machine.num_xcds
         else:
-            workers = topo.num_sms - 1
+            workers = (ctas or topo.num_sms) - 1
             n_dies = 1
         if lm_tile is None:
             lm_tile = _default_lm_tile(self.spec, g.batch)
@@ -243,6 +258,13 @@ class Megakernel:
             self.state.kpart = torch.zeros(n_dies * workers * 2 * PIECE_FLOATS,
                                            device=f"cuda:{device}", dtype=torch.float32)
         opts.ksplit = ksplit
+        if self.tp[1] > 1:
+            from .lowering import TPLayout
+            layout = TPLayout(self.tp[1], g.batch, self.spec.hidden, len(self.state.layers))
+            ptr = C.c_void_p()
+            L.check(self.lib.mk_tp_alloc(device, layout.nbytes, C.byref(ptr)))
+            self.tp_region, self.tp_layout = ptr.value, layout
+            opts.tp_rank, opts.tp_world, opts.tp_layout = self.tp[0], self.tp[1], layout
         self.lowered = lower(g, self.spec, self.state, opts)
         run_topo = topo if per_die else flat_topology(topo.num_sms)
         # KV cache row layout the lowered attention reads and appends: the
@@ -255,6 +277,8 @@ class Megakernel:
         L.check(self.lib.mk_create(device, C.byref(self._desc), C.byref(run_topo),
                                    C.byref(h)))
         self.h = h
+        if ctas is not None or not cooperative:
+            L.check(self.lib.mk_set_grid(self.h, ctas or topo.num_sms, 1 if cooperative else 0))
         L.check(self.lib.mk_set_watchdog(self.h, watchdog_s))
         L.check(self.lib.mk_set_prefetch(self.h, int(os.environ.get("MK_PREFETCH", "0"))))
         self.steps = 0
@@ -398,10 +422,22 @@ class Megakernel:
             L.check(-got)
         return buf.reshape(-1, self._trace_cap, 8)
 
+    def tp_connect(self, peer_bases):
+        """mk_tp_init: ``peer_bases[q]`` = rank q's exchange region as
+        addressable from this device (own region at index rank)."""
+        arr = (C.c_void_p * len(peer_bases))(*peer_bases)
+        L.check(self.lib.mk_tp_init(self.h, self.tp[0], self.tp[1], arr))
+
     def close(self):
         if getattr(self, "h", None):
             self.lib.mk_destroy(self.h)
             self.h = None
+        for p in getattr(self, "tp_opened", []):
+            self.lib.mk_ipc_close(C.c_void_p(p))
+        self.tp_opened = []
+        if getattr(self, "tp_region", None):
+            self.lib.mk_tp_free(C.c_void_p(self.tp_region))
+            self.tp_region = None
 
     def __del__(self):
         try:

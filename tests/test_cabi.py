@@ -45,7 +45,7 @@ def test_struct_layouts_match_header(tmp_path):
                "mk_gemm_params": L.GemmParams, "mk_norm_params": L.NormParams,
                "mk_attn_params": L.AttnParams, "mk_silu_params": L.SiluParams,
                "mk_argmax_params": L.ArgmaxParams, "mk_graph_desc": L.GraphDesc,
-               "mk_counters": L.Counters, "mk_log_rec": L.LogRec}
+               "mk_counters": L.Counters, "mk_log_rec": L.LogRec, "mk_tp_params": L.TPParams}
     src = tmp_path / "sz.c"
     body = "".join(f'printf("{n} %zu\\n", sizeof({n}));' for n in structs)
     src.write_text('#include <stdio.h>\n#include "mk.h"\nint main(void){' + body + "return 0;}\n")
