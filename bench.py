@@ -18,8 +18,12 @@ copied host->device and the greedy ids device->host every step.
 reference path restated; the reference package itself has no numerics) on a
 bounded sample on the host cores.
 
-Multi-GPU (torchrun): replicas only in this round -- every rank decodes its
-own batch; value = all ranks' tokens / max-over-ranks time ("weak" scaling).
+Multi-GPU (torchrun): by default replicas -- every rank decodes its own
+batch; value = all ranks' tokens / max-over-ranks time ("weak" scaling).
+``--tp``: the ranks form one Megatron tensor-parallel group decoding ONE
+batch (per-layer allreduces as device tasks over NVLink peer memory, CUDA
+IPC bootstrap) -- "strong" scaling.  ``--tp-emulate N`` (1 GPU): N TP ranks
+share the GPU on disjoint SM subsets (the device TP data path, measured).
 """
 
 from __future__ import annotations
@@ -275,6 +279,121 @@ def run_ours(args):
     mk.close()
 
 
+def build_tp(args, device, rank, world, emulate):
+    """One Megakernel per TP rank: ``emulate`` = all ranks on this GPU (flat
+    scheduler, #SMs / world CTAs each), else this process's rank on its own
+    GPU (per-die scheduler) joined through CUDA IPC."""
+    import torch
+    from dataclasses import replace
+    from paper_2604_15379_b200 import b200_from_probe, build_decoder_layer, model_preset
+    from paper_2604_15379_b200 import dist as D
+    from paper_2604_15379_b200.analytics import device_tiles
+    from paper_2604_15379_b200.runtime import Megakernel, halves_topology, probe, topology_summary
+    from paper_2604_15379_b200.weights import Qwen3Spec, Qwen3Weights
+    topo = probe(device)
+    if topo.num_dies != 2:
+        topo = halves_topology(topo.num_sms)
+    model = replace(model_preset("qwen3-8b"), num_layers=args.layers)
+    spec = Qwen3Spec.qwen3_8b(layers=args.layers)
+    w = Qwen3Weights.random(spec, seed=0, device=f"cuda:{device}")
+    t_max = CTX + 2 * (args.warmup + args.steps) + 64
+    if emulate:
+        ctas = topo.num_sms // world
+        mach = b200_from_probe([ctas])
+        kw = dict(sched="flat", ctas=ctas, cooperative=False)
+        ranks = range(world)
+    else:
+        mach = b200_from_probe([topo.sms_per_die[i] for i in range(topo.num_dies)])
+        kw = dict(sched="per_die")
+        ranks = [rank]
+    g = build_decoder_layer(model, mach, "chiplet", args.batch,
+                            tile_overrides=device_tiles(model, mach, "chiplet", args.batch,
+                                                        tp=world), layers=args.layers)
+    mks = [Megakernel(g, w, t_max=t_max, topo=topo, keep_logits=False, device=device,
+                      tp=(r, world), **kw) for r in ranks]
+    del w
+    torch.cuda.empty_cache()
+    if emulate:
+        D.connect_local(mks)
+    else:
+        D.connect_dist(mks[0])
+    for mk in mks:
+        mk.fill_kv_random(CTX)
+        mk.set_tokens([(17 * i + 3) % VOCAB for i in range(args.batch)])
+    info = {"topology": topology_summary(topo), "graph_tasks": len(g.tasks),
+            "units": len(mks[0].lowered.units), "tp": world,
+            "tp_placement": f"{world} ranks on one GPU, {topo.num_sms // world} SMs each"
+                            if emulate else "one rank per GPU (CUDA IPC peer regions)"}
+    return mks, model, info
+
+
+def run_tp(args):
+    import torch
+    from paper_2604_15379_b200.analytics import decode_step_bytes
+    from paper_2604_15379_b200.dist import allreduce_bytes_per_step
+    emulate = args.tp_emulate > 1
+    rank, world, local = dist_setup(args.gpus) if not emulate else (0, 1, 0)
+    tp = args.tp_emulate if emulate else world
+    torch.cuda.set_device(local)
+    mks, model, info = build_tp(args, local, rank, tp, emulate)
+    streams = [torch.cuda.Stream() for _ in mks]
+    main = torch.cuda.current_stream()
+
+    def steps(n):
+        ev = torch.cuda.Event()
+        ev.record(main)
+        for st in streams:
+            st.wait_event(ev)
+        for _ in range(n):
+            for mk, st in zip(mks, streams):
+                mk.launch(stream=st)
+        for st in streams:
+            e = torch.cuda.Event()
+            e.record(st)
+            main.wait_event(e)
+
+    steps(args.warmup)
+    for mk in mks:
+        mk.sync()
+    barrier(world)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(main)
+        steps(args.steps)
+        ev1.record(main)
+        torch.cuda.synchronize()
+    for mk in mks:
+        mk.sync()
+    ms = max_over_ranks(ev0.elapsed_time(ev1), world)
+    ms_step = ms / args.steps
+    B = args.batch
+    tokens = [mk.state.out_tokens.cpu() for mk in mks]
+    same = all(torch.equal(t, tokens[0]) for t in tokens)
+    bytes_step = decode_step_bytes(model, B, CTX, VOCAB)
+    ar = allreduce_bytes_per_step(mks[0].spec, B, 4)
+    line = {
+        "metric": METRIC, "value": round(B / (ms_step / 1e3), 3), "unit": "tok/s",
+        "n_gpus": 1 if emulate else world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (hash-init bf16 weights, synthetic 1024-token bf16 KV)",
+        "config": {"workload": f"Qwen3-8B decode, batch {B}, ctx {CTX}, TP={tp} megakernel",
+                   "parallelism": f"tp{tp}", "batch": B, "ctx": CTX, "layers": model.num_layers,
+                   "ranks_agree_on_tokens": same,
+                   "allreduce_fp32_bytes_per_step": ar["bytes_per_step"] * tp, **info},
+        "roofline": {"bound": "hbm", "algorithmic_bytes_per_step": bytes_step["total"],
+                     "achieved": round(bytes_step["total"] / (ms_step / 1e3) / 1e9, 1),
+                     "unit": "GB/s (all ranks)"},
+        "gpu_launches": args.steps * len(mks),
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    for mk in mks:
+        mk.close()
+
+
 def _profiled_traffic(args):
     """dram bytes per launch from a committed ncu --set full capture, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -375,6 +494,10 @@ def main():
     ap.add_argument("--t-m", type=int, default=None,
                     help="batch rows per m-tile (default: 16 for the GEMV body, "
                          "the whole batch up to 64 for tcgen05)")
+    ap.add_argument("--tp", action="store_true",
+                    help="torchrun ranks form one tensor-parallel group (default: replicas)")
+    ap.add_argument("--tp-emulate", type=int, default=0,
+                    help="N tensor-parallel ranks sharing this one GPU")
     ap.add_argument("--no-ksplit", action="store_true",
                     help="die tasks own whole tiles per schedule() (no K-split)")
     args = ap.parse_args()
@@ -383,7 +506,10 @@ def main():
     if args.impl == "reference":
         run_reference(args)
     else:
-        run_ours(args)
+        if args.tp or args.tp_emulate > 1:
+            run_tp(args)
+        else:
+            run_ours(args)
 
 
 if __name__ == "__main__":
