@@ -201,6 +201,12 @@ typedef struct mk_attn_params {
                           splits into `out` (per-row arrival counters at
                           red_ctr0); ATTN_REDUCE: no-op                    */
   int32_t red_ctr0;    /* first per-row arrival sub-counter                 */
+  const int32_t* page_table; /* paged KV (NULL = contiguous rows): [M][max_pages]
+                          physical page of every `split`-token block of a row;
+                          k_cache / v_cache are then page pools
+                          [n_pages][kv_heads][split][head_dim]            */
+  int32_t max_pages;   /* pages per row (t_max / split)                     */
+  int32_t pad;
 } mk_attn_params;
 
 typedef struct mk_silu_params {

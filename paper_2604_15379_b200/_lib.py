@@ -72,7 +72,8 @@ class AttnParams(C.Structure):
                 ("head_dim", I32), ("group", I32), ("kv_head", I32),
                 ("split", I32), ("n_splits", I32), ("t_max", I32),
                 ("eps", F32), ("scale", F32), ("sub_splits", I32), ("mma", I32),
-                ("fuse_reduce", I32), ("red_ctr0", I32)]
+                ("fuse_reduce", I32), ("red_ctr0", I32), ("page_table", P),
+                ("max_pages", I32), ("pad", I32)]
 
 
 class SiluParams(C.Structure):

@@ -324,6 +324,17 @@ __device__ __forceinline__ const T* P(const KArgs& a, const mk_task& t) {
   return reinterpret_cast<const T*>(s.pcache[&t - s.tcache]);
 }
 
+// Element offset of token `tok`'s row (kv head p.kv_head, sequence b) in the
+// KV cache: contiguous [M][kv_heads][t_max][hd], or -- paged KV -- the
+// row's page of `split` tokens in the pool [n_pages][kv_heads][split][hd].
+__device__ __forceinline__ size_t kv_off(const mk_attn_params& p, int b, int tok) {
+  if (p.page_table) {
+    const int pg = p.page_table[size_t(b) * p.max_pages + tok / p.split];
+    return ((size_t(pg) * p.kv_heads + p.kv_head) * p.split + tok % p.split) * p.head_dim;
+  }
+  return ((size_t(b) * p.kv_heads + p.kv_head) * p.t_max + tok) * p.head_dim;
+}
+
 // MK_EPI_PARTIAL: one fp32 partial-product element pushed into every rank's
 // exchange region (this rank's slot: byte offset p.y, row-major [M][ldy]).
 // Remote stores are posted over NVLink; the unit fences at system scope
@@ -553,8 +564,7 @@ struct SlotIter {
       if (t0 > pos) continue;
       const int nc = full ? p.split : min(p.split, pos - t0);
       if (nc <= 0) continue;
-      const size_t row = (size_t(b) * p.kv_heads + p.kv_head) * p.t_max + t0;
-      src_k = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + row * p.head_dim;
+      src_k = reinterpret_cast<const __nv_bfloat16*>(p.k_cache) + kv_off(p, b, t0);
       bytes_kv = uint32_t(nc) * p.head_dim * 2;
       src = src_k; bytes = bytes_kv; kv = 1;
       return true;
@@ -2108,7 +2118,7 @@ __device__ void attn_pass(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
 #pragma unroll
     for (int e = 0; e < 8; ++e) { kb[e] = f2bf(kn[e]); kn[e] = bf2f(kb[e]); }   // attend to the cached key
     if (head == 0 && sub == 0 && tg == 0) {
-      const size_t crow = ((size_t(b) * p.kv_heads + p.kv_head) * p.t_max + pos) * HD + dl * 8;
+      const size_t crow = kv_off(p, b, pos) + dl * 8;
       *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.k_cache) + crow) = *reinterpret_cast<uint4*>(kb);
       *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.v_cache) + crow) = vv;
     }
@@ -2270,7 +2280,7 @@ __device__ __forceinline__ void attn_mma_tokens(const KArgs& a, Smem& s, uint8_t
       }
       const uint32_t off = kv_swz(nt, dl);
       *reinterpret_cast<uint4*>((half == 0 ? kslot : vslot) + off) = kv4;
-      const size_t crow = ((size_t(b) * p.kv_heads + p.kv_head) * p.t_max + pos) * kAttnHD;
+      const size_t crow = kv_off(p, b, pos);
       uint16_t* cache = reinterpret_cast<uint16_t*>(half == 0 ? p.k_cache : p.v_cache);
       *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(cache + crow) + ((dl ^ (pos & 7)) << 4)) = kv4;
     }
@@ -3576,7 +3586,8 @@ static int validate_graph(const mk_graph_desc* g) {
                              : (p->group * p->sub_splits <= kConsWarps && kConsWarps % (p->group * p->sub_splits) == 0);
       if ((hd != 16 && hd != 32 && hd != 64 && hd != 128) || p->group < 1 || p->group > 8 ||
           8 % p->group || size_t(p->split) * hd * 2 > size_t(kSlotBytes) ||
-          p->n_splits > kMaxSplits || p->sub_splits < 1 || !ws_ok || (mma && p->t_max % kAttnSplit))
+          p->n_splits > kMaxSplits || p->sub_splits < 1 || !ws_ok || (mma && p->t_max % kAttnSplit) ||
+          (p->page_table && p->max_pages * p->split != p->t_max))
         return fail(MK_ERR_CONFIG, "attention task " + std::to_string(i) + " has unsupported shapes");
     }
   }

@@ -321,6 +321,9 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         p.rope_cos, p.rope_sin = _ptr(bufs.rope_cos), _ptr(bufs.rope_sin)
         p.positions = _ptr(bufs.positions)
         p.partial = _ptr(bufs.partial)
+        if getattr(bufs, "page_table", None) is not None:       # paged KV pools
+            p.page_table = _ptr(bufs.page_table)
+            p.max_pages = bufs.page_table.shape[1]
         p.out = _ptr(out)
         p.M, p.ldqkv = B, spec.qkv_dim
         p.q_heads, p.kv_heads, p.head_dim = spec.q_heads, spec.kv_heads, hd

@@ -117,11 +117,16 @@ class DeviceState:
     rope_cos: torch.Tensor = None
     rope_sin: torch.Tensor = None
     vocab_pad: int = 0
+    page_table: torch.Tensor = None
 
 
 def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
                 amax_slots: int, device="cuda", split: int | None = None,
-                keep_logits: bool = True) -> DeviceState:
+                keep_logits: bool = True, kv_pages: int | None = None) -> DeviceState:
+    """Device buffers of one lowered graph.  ``kv_pages``: paged KV -- every
+    layer's K and V become pools of ``kv_pages`` pages of ``split`` tokens
+    ([pages][kv_heads][split][head_dim]) addressed through a per-row page
+    table ([B][t_max / split] int32, Megakernel assigns pages)."""
     g = adopt_graph(g)
     sp = weights.spec
     B = g.batch
@@ -169,8 +174,9 @@ def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
             "silu_out": torch.zeros(B, sp.ffn, **bf),
             "x_out": torch.zeros(B, sp.hidden, **bf),
         })
-        st.k_cache.append(torch.zeros(B, sp.kv_heads, t_max, hd, **bf))
-        st.v_cache.append(torch.zeros(B, sp.kv_heads, t_max, hd, **bf))
+        kv_shape = (kv_pages, sp.kv_heads, split, hd) if kv_pages else (B, sp.kv_heads, t_max, hd)
+        st.k_cache.append(torch.zeros(*kv_shape, **bf))
+        st.v_cache.append(torch.zeros(*kv_shape, **bf))
     del w.layers[:]
     _, tn, tk = lm_tile
     if is_umma_tile(lm_tile, False):
@@ -193,9 +199,28 @@ def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
     st.tokens = torch.zeros(B, device=dev, dtype=torch.int32)
     st.out_tokens = torch.zeros(B, device=dev, dtype=torch.int32)
     st.positions = torch.zeros(B, device=dev, dtype=torch.int32)
+    st.page_table = torch.zeros(B, n_splits, device=dev, dtype=torch.int32) if kv_pages else None
     cos, sin = rope_tables(hd, sp.rope_theta, t_max)
     st.rope_cos, st.rope_sin = cos.to(dev), sin.to(dev)
     return st
+
+
+class PagePool:
+    """Free list of KV pages (paged KV): pages are handed out in an
+    interleaved order, so a row's pages are in general not contiguous."""
+
+    def __init__(self, n_pages: int):
+        order = list(range(0, n_pages, 2)) + list(range(1, n_pages, 2))
+        self.free = order[::-1]
+        self.n_pages = n_pages
+
+    def alloc(self) -> int:
+        if not self.free:
+            raise L.MkError(L.MK_ERR_CONFIG, "KV page pool exhausted")
+        return self.free.pop()
+
+    def release(self, pages):
+        self.free.extend(int(p) for p in pages if p >= 0)
 
 
 class Megakernel:
@@ -209,13 +234,16 @@ class Megakernel:
                  keep_logits: bool = True, watchdog_s: float = 10.0,
                  ksplit: bool = True, fuse_attn_reduce: bool = False,
                  tp: tuple | None = None, ctas: int | None = None,
-                 cooperative: bool = True):
+                 cooperative: bool = True, kv_pages: int | None = None):
         """``tp=(rank, world)``: this rank's shard of a Megatron tensor-
         parallel group (``weights`` are the full model; dist.shard_weights
         slices them); join the group with dist.connect_local /
         dist.connect_dist before the first step.  ``ctas`` (flat scheduler
         only) launches that many CTAs -- several ranks can then share one GPU
-        on disjoint SMs (``cooperative=False``: plain launches)."""
+        on disjoint SMs (``cooperative=False``: plain launches).
+        ``kv_pages``: paged KV cache with a pool of that many pages of one
+        attention split (64 tokens on the tensor-core path) per layer; pages
+        are assigned as rows advance and returned by release_row()."""
         if not torch.cuda.is_available():
             raise RuntimeError("Megakernel needs a CUDA device (no CPU fallback)")
         self.lib = L.load()
@@ -252,7 +280,10 @@ class Megakernel:
         amax_slots = (n_dies * workers) if per_die else v_pad // lm_tile[1]
         self.state = build_state(g, weights, t_max, lm_tile, amax_slots,
                                  device=f"cuda:{device}",
-                                 keep_logits=keep_logits)
+                                 keep_logits=keep_logits, kv_pages=kv_pages)
+        self.pool = PagePool(kv_pages) if kv_pages else None
+        if self.pool:
+            self._table = torch.full((g.batch, self.state.n_splits), -1, dtype=torch.int32)
         if per_die and ksplit:
             # K-split pieces: [die][worker][first/last segment][128 x 64] fp32
             self.state.kpart = torch.zeros(n_dies * workers * 2 * PIECE_FLOATS,
@@ -295,6 +326,60 @@ class Megakernel:
             raise ValueError(f"positions must lie in [0, t_max={self.state.t_max})")
         self._pos = pos.clone()
         self.state.positions.copy_(pos.to(torch.int32))
+        self._ensure_pages(self._pos)
+
+    # ---- paged KV ------------------------------------------------------------
+    def _ensure_pages(self, upto):
+        """Every row holds pages for tokens [0, upto[b]] (the next append)."""
+        if not self.pool:
+            return
+        S = self.state.split
+        dirty = False
+        for b in range(self.graph.batch):
+            for i in range(int(upto[b]) // S + 1):
+                if i < self._table.shape[1] and self._table[b, i] < 0:
+                    self._table[b, i] = self.pool.alloc()
+                    dirty = True
+        if dirty:
+            self.state.page_table.copy_(self._table.clamp(min=0))
+
+    def release_row(self, b: int):
+        """Sequence in row ``b`` finished: its KV pages go back to the pool and
+        the row restarts at position 0 (continuous batching)."""
+        if self.pool:
+            self.pool.release(self._table[b].tolist())
+            self._table[b] = -1
+        self._pos[b] = 0
+        self.state.positions[b] = 0
+        self._ensure_pages(self._pos)
+
+    def page_table(self) -> torch.Tensor:
+        """Host copy of the page table ([B][t_max / split], -1 = unassigned)."""
+        return self._table.clone() if self.pool else None
+
+    def _logical(self, buf: torch.Tensor, n: int) -> torch.Tensor:
+        """[B, kvh, n, hd] logical view (a copy when paged)."""
+        if not self.pool:
+            return buf[:, :, :n]
+        S = self.state.split
+        rows = []
+        for b in range(self.graph.batch):
+            blocks = [buf[int(self._table[b, i])] for i in range(-(-n // S))]
+            rows.append(torch.cat(blocks, 1)[:, :n])
+        return torch.stack(rows)
+
+    def _store_logical(self, buf: torch.Tensor, x: torch.Tensor):
+        """Write [B, kvh, n, hd] into tokens [0, n) of every row."""
+        n = x.shape[2]
+        if not self.pool:
+            buf[:, :, :n] = x
+            return
+        self._ensure_pages([n - 1] * self.graph.batch)
+        S = self.state.split
+        for b in range(self.graph.batch):
+            for i in range(-(-n // S)):
+                c = min(S, n - i * S)
+                buf[int(self._table[b, i]), :, :c] = x[b, :, i * S:i * S + c]
 
     def positions(self) -> torch.Tensor:
         """Host copy of the decode position of every row (the next token's index)."""
@@ -325,13 +410,13 @@ class Megakernel:
                 out = torch.empty_like(x).view(B, H, n, hd // 8, 8)
                 out.scatter_(3, idx.expand(B, H, n, hd // 8, 8), x.view(B, H, n, hd // 8, 8))
                 x = out.view(B, H, n, hd)
-            dst[:, :, :n_tokens] = x
+            self._store_logical(dst, x)
 
     def read_kv(self, layer: int, n_tokens: int):
         """Canonical (un-swizzled) copies of tokens [0, n_tokens) of the cache."""
         out = []
         for buf in (self.state.k_cache[layer], self.state.v_cache[layer]):
-            x = buf[:, :, :n_tokens]
+            x = self._logical(buf, n_tokens)
             if self.kv_swizzled:
                 B, H, n, hd = x.shape
                 idx = self._swizzle_index(n, x.device).view(1, 1, n, hd // 8, 1)
@@ -342,13 +427,13 @@ class Megakernel:
 
     def fill_kv_random(self, n_tokens: int, seed: int = 99):
         """Perf runs: ``n_tokens`` of synthetic bf16 context per sequence."""
+        sp = self.spec
+        shape = (self.graph.batch, sp.kv_heads, n_tokens, sp.head_dim)
         for li, (k, v) in enumerate(zip(self.state.k_cache, self.state.v_cache)):
             for j, buf in enumerate((k, v)):
-                n = buf[:, :, :n_tokens].numel()
-                u = hash_uniform(n, seed, 2 * li + j, device=buf.device)
+                u = hash_uniform(int(torch.Size(shape).numel()), seed, 2 * li + j, device=buf.device)
                 # i.i.d. values: the swizzled layout is a permutation of them
-                buf[:, :, :n_tokens] = ((u * 2 - 1) * 1.7).to(torch.bfloat16).view(
-                    buf[:, :, :n_tokens].shape)
+                self._store_logical(buf, ((u * 2 - 1) * 1.7).to(torch.bfloat16).view(shape))
         self.set_positions([n_tokens] * self.graph.batch)
 
     # ---- execution ---------------------------------------------------------
@@ -358,6 +443,7 @@ class Megakernel:
         if int(self._pos.max()) >= self.state.t_max:
             raise L.MkError(L.MK_ERR_CONFIG, f"decode position {int(self._pos.max())} "
                             f"reached t_max={self.state.t_max}")
+        self._ensure_pages(self._pos)           # paged KV: the page this append lands in
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         L.check(self.lib.mk_step(self.h, C.c_void_p(s.cuda_stream)))
         self._pos += 1                          # the argmax task advances the positions
@@ -373,6 +459,37 @@ class Megakernel:
         self.launch()
         self.sync()
         return self.state.out_tokens.clone()
+
+    def generate(self, prompts, max_new_tokens: int = 1):
+        """Device prefill + greedy decode for ragged prompts (one list of
+        token ids per row, any lengths >= 1).  Every row starts at position
+        0; step t feeds row b its prompt token t while the prompt lasts, then
+        its own previous greedy token, so each row's KV context is built on
+        the device by the decode kernels themselves.  Returns, per row, the
+        ``max_new_tokens`` greedy tokens that follow its prompt."""
+        B = self.graph.batch
+        if len(prompts) != B or min(len(p) for p in prompts) < 1:
+            raise ValueError(f"need {B} non-empty prompts")
+        lens = [len(p) for p in prompts]
+        total = max(n + max_new_tokens - 1 for n in lens)
+        if total > self.state.t_max:
+            raise ValueError(f"{total} positions exceed t_max={self.state.t_max}")
+        for b in range(B):
+            self.release_row(b)
+        outs = [[] for _ in range(B)]
+        prev = [0] * B
+        for t in range(total):
+            toks = [prompts[b][t] if t < lens[b] else prev[b] for b in range(B)]
+            prev = self.step(toks).cpu().tolist()
+            for b in range(B):
+                if t >= lens[b] - 1 and len(outs[b]) < max_new_tokens:
+                    outs[b].append(prev[b])
+        return outs
+
+    def prefill(self, prompts):
+        """Build every row's KV context from its prompt on the device;
+        returns the greedy token after each prompt."""
+        return [o[0] for o in self.generate(prompts, 1)]
 
     def logits(self):
         lg = self.state.logits
