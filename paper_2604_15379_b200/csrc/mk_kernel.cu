@@ -639,17 +639,36 @@ __device__ void stage_x(const KArgs& a, Smem& s, const mk_gemm_params& p, int m0
       gv[q] = (norm && k < K) ? *reinterpret_cast<const uint4*>(gs + k) : make_uint4(0, 0, 0, 0);
     }
     if (norm) {
+      // RMSNorm as a post-scale: stage gamma * x (one pass, no statistics
+      // barrier before it) and the per-warp sums of squares; the GEMV
+      // epilogue multiplies each row's dot products by its 1/rms
+      // (post_rs) -- y = rs * W (gamma . x), the model's math without the
+      // intermediate bf16 rounding of x * rs.
+      const int warp = ct >> 5, lane = ct & 31;
 #pragma unroll
       for (int b = 0; b < kMaxNB; ++b) {
         if (b < rows) {
-          for (int k = ct * 8; k < K; k += kCons * 8) {
-            float f[8];
-            unpack8(*reinterpret_cast<const uint4*>(&s.u.xs[b * K + k]), f);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) ss[b] = fmaf(f[e], f[e], ss[b]);
+          for (int q = 0; q < kSeg; ++q) {
+            const int k = ct * 8 + q * kCons * 8;
+            if (k >= K) continue;
+            float f[8], g[8];
+            unpack8(*reinterpret_cast<const uint4*>(&s.u.xs[b * K + k]), f);
+            unpack8(gv[q], g);
+            uint16_t o[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) { ss[b] = fmaf(f[e], f[e], ss[b]); o[e] = f2bf(g[e] * f[e]); }
+            *reinterpret_cast<uint4*>(&s.u.xs[b * K + k]) = *reinterpret_cast<uint4*>(o);
           }
+          float v = ss[b];
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+          if (lane == 0) s.rsum[warp][b] = v;
         }
       }
+      if (trace && ct == 0 && s.tr[7] == 0) s.tr[7] = globaltimer();
+      bar_sync(1, kCons);
+      return;
     }
   } else {
     // gamma is static: issue its loads together with x's (one round trip)
@@ -712,6 +731,17 @@ __device__ void stage_x(const KArgs& a, Smem& s, const mk_gemm_params& p, int m0
     }
   }
   bar_sync(1, kCons);
+}
+
+// 1/rms of staged row b when stage_x normalised by post-scale (hoisted
+// staging with a norm), else 1 (rows pre-normalised or no norm).  The
+// per-warp sums of squares were written before stage_x's final barrier.
+__device__ __forceinline__ float post_rs(const Smem& s, const mk_gemm_params& p, int b) {
+  if (!p.norm_gamma || !s.xs_hoist) return 1.f;
+  float t = 0.f;
+#pragma unroll
+  for (int w = 0; w < kConsWarps; ++w) t += s.rsum[w][b];
+  return rsqrtf(t / float(p.K) + p.norm_eps);
 }
 
 // K-split piece handling for the CUDA-core body.  Called by all consumer
@@ -850,6 +880,11 @@ __device__ void gemm_tile(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     if (lane != b || b >= rows_m) continue;
+    if (p.norm_gamma) {                 // post-scale RMSNorm (stage_x)
+      const float r = post_rs(s, p, b);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) if (j < rpw) acc[j][b] *= r;
+    }
     if (p.epilogue == MK_EPI_LOGITS) {
       float* y = reinterpret_cast<float*>(p.y);
 #pragma unroll
@@ -988,6 +1023,11 @@ __device__ void gemm_tile_fast(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     if (lane != b || b >= rows_m) continue;
+    if (p.norm_gamma) {                 // post-scale RMSNorm (stage_x)
+      const float r = post_rs(s, p, b);
+#pragma unroll
+      for (int j = 0; j < RPW; ++j) tot[j][b] *= r;
+    }
     if (p.epilogue == MK_EPI_LOGITS) {
       float* y = reinterpret_cast<float*>(p.y);
 #pragma unroll
@@ -1125,6 +1165,11 @@ __device__ __forceinline__ void gemm_tile_fast_ks(const KArgs& a, Smem& s, uint8
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     if (lane != b || b >= rows_m) continue;
+    if (p.norm_gamma) {                 // post-scale RMSNorm (stage_x)
+      const float r = post_rs(s, p, b);
+#pragma unroll
+      for (int j = 0; j < RPW; ++j) tot[j][b] *= r;
+    }
     if (p.epilogue == MK_EPI_LOGITS) {
       float* y = reinterpret_cast<float*>(p.y);
 #pragma unroll
