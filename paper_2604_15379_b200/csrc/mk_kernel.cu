@@ -909,13 +909,13 @@ __device__ void gemm_tile(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
           if (j >= rpw / 2) continue;
           const float g = acc[j][b];
           const float u = rpw == 2 ? acc[1][b] : (j == 0 ? acc[2][b] : acc[3][b]);
-          y[out_col0 + warp + kConsWarps * j] = f2bf(g / (1.f + __expf(-g)) * u);
+          st_out(&y[out_col0 + warp + kConsWarps * j], f2bf(g / (1.f + __expf(-g)) * u));
         }
       } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           if (j >= rpw) continue;
-          y[out_col0 + warp + kConsWarps * j] = f2bf(acc[j][b] + resv[j]);
+          st_out(&y[out_col0 + warp + kConsWarps * j], f2bf(acc[j][b] + resv[j]));
         }
       }
     }
@@ -1047,12 +1047,12 @@ __device__ void gemm_tile_fast(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
 #pragma unroll
           for (int j = 0; j < RPW / 2; ++j) {
             const float g = tot[j][b], u = tot[j + RPW / 2][b];
-            y[out_col0 + warp + kConsWarps * j] = f2bf(g / (1.f + __expf(-g)) * u);
+            st_out(&y[out_col0 + warp + kConsWarps * j], f2bf(g / (1.f + __expf(-g)) * u));
           }
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < RPW; ++j) y[out_col0 + warp + kConsWarps * j] = f2bf(tot[j][b] + resv[j]);
+        for (int j = 0; j < RPW; ++j) st_out(&y[out_col0 + warp + kConsWarps * j], f2bf(tot[j][b] + resv[j]));
       }
     }
   }
@@ -1189,12 +1189,12 @@ __device__ __forceinline__ void gemm_tile_fast_ks(const KArgs& a, Smem& s, uint8
 #pragma unroll
           for (int j = 0; j < RPW / 2; ++j) {
             const float g = tot[j][b], u = tot[j + RPW / 2][b];
-            y[out_col0 + warp + kConsWarps * j] = f2bf(g / (1.f + __expf(-g)) * u);
+            st_out(&y[out_col0 + warp + kConsWarps * j], f2bf(g / (1.f + __expf(-g)) * u));
           }
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < RPW; ++j) y[out_col0 + warp + kConsWarps * j] = f2bf(tot[j][b] + resv[j]);
+        for (int j = 0; j < RPW; ++j) st_out(&y[out_col0 + warp + kConsWarps * j], f2bf(tot[j][b] + resv[j]));
       }
     }
   }
@@ -1614,7 +1614,7 @@ __device__ __forceinline__ void umma_epi16(const KArgs& a, Smem& s, const mk_gem
       const float u = __shfl_down_sync(0xffffffffu, v[i], 16);
       const int bi = 16 * j + i;
       if (lane < 16 && bi < rows_m)
-        y[size_t(m0 + bi) * p.ldy + col] = f2bf(v[i] / (1.f + __expf(-v[i])) * u);
+        st_out(&y[size_t(m0 + bi) * p.ldy + col], f2bf(v[i] / (1.f + __expf(-v[i])) * u));
     }
   } else {
     uint16_t* y = reinterpret_cast<uint16_t*>(p.y);
@@ -1629,7 +1629,7 @@ __device__ __forceinline__ void umma_epi16(const KArgs& a, Smem& s, const mk_gem
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int bi = 16 * j + i;
-      if (bi < rows_m) y[size_t(m0 + bi) * p.ldy + col] = f2bf(v[i] + rv[i]);
+      if (bi < rows_m) st_out(&y[size_t(m0 + bi) * p.ldy + col], f2bf(v[i] + rv[i]));
     }
   }
 }

@@ -161,6 +161,13 @@ __device__ __forceinline__ uint4 ldg128_cg(const void* p) {
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
   return v;
 }
+// GEMM output element (the reference's NON_TEMPORAL output store role,
+// traversal.py:296-313): not allocated in the producing SM's L1 -- the
+// consumers are other SMs and read it from L2, the GPU's coherence point
+__device__ __forceinline__ void st_out(uint16_t* p, uint16_t v) {
+  asm volatile("st.global.L1::no_allocate.b16 [%0], %1;" :: "l"(p), "h"(v) : "memory");
+}
+
 // small static operands (norm gammas, RoPE tables): keep them L2-resident
 // while the weight stream (evict_first) passes through
 __device__ __forceinline__ uint64_t policy_evict_last() {
