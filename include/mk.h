@@ -159,8 +159,14 @@ typedef struct mk_gemm_params {
                          schedule() (traversal.py:125-202)             */
   int32_t tile_ctr0;  /* K-split: first per-tile arrival sub-counter      */
   int32_t piece_floats;/* K-split: floats per partial piece               */
-  int32_t pad2;
+  int32_t ss_nparts;  /* tcgen05 folded RMSNorm: partial sums per row in ss_in */
   float* kpart;       /* K-split: partial pieces [W][2][piece_floats] fp32 */
+  float* ss_out;      /* tcgen05 residual epilogue: per (128-col tile, TMEM
+                         quadrant) sums of squares of the bf16 output,
+                         [d/128*4][M] -- the next RMSNorm's statistics     */
+  const float* ss_in; /* tcgen05 GEMM after an RMSNorm folded into its
+                         weights (W * gamma): [ss_nparts][M] partials; the
+                         epilogue scales row b by rsqrt(sum/K + eps)       */
 } mk_gemm_params;
 
 typedef struct mk_norm_params {
@@ -173,6 +179,7 @@ typedef struct mk_norm_params {
   int32_t M, d;
   float eps;
   int32_t fused;       /* 1: the consuming GEMM normalises; only gather here */
+  float* ss_out;       /* fused + L0 gather: each row's sum of squares [M]   */
 } mk_norm_params;
 
 typedef struct mk_attn_params {

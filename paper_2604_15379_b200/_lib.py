@@ -56,12 +56,13 @@ class GemmParams(C.Structure):
                 ("amax_base", I32), ("amax_stride", I32), ("stage_x", I32),
                 ("norm_eps", F32), ("body", I32), ("y_cols", I32),
                 ("ksplit", I32), ("tile_ctr0", I32), ("piece_floats", I32),
-                ("pad2", I32), ("kpart", P)]
+                ("ss_nparts", I32), ("kpart", P), ("ss_out", P), ("ss_in", P)]
 
 
 class NormParams(C.Structure):
     _fields_ = [("x", P), ("gamma", P), ("y", P), ("embed", P), ("tokens", P),
-                ("x_store", P), ("M", I32), ("d", I32), ("eps", F32), ("fused", I32)]
+                ("x_store", P), ("M", I32), ("d", I32), ("eps", F32), ("fused", I32),
+                ("ss_out", P)]
 
 
 class AttnParams(C.Structure):

@@ -163,6 +163,7 @@ struct Smem {
   int ibred[32];
   float rsum[kConsWarps][kMaxNB];   // x-staging: per-warp sums of squares
   float rs[kMaxNB];                 // x-staging: 1/rms per staged row
+  float rsn[kAmaxRows];             // tcgen05 folded RMSNorm: 1/rms per batch row
   int4 cur;                         // consumer broadcast: current unit
   int abort_flag;
   int piece_last;                   // K-split: this CTA summed the tile's pieces (GEMV)
@@ -1626,10 +1627,27 @@ __device__ __forceinline__ void umma_epi16(const KArgs& a, Smem& s, const mk_gem
     } else {
       umma_res16(p, m0, rows_m, col, j, rv);
     }
+    float sq[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int bi = 16 * j + i;
-      if (bi < rows_m) st_out(&y[size_t(m0 + bi) * p.ldy + col], f2bf(v[i] + rv[i]));
+      const uint16_t o = f2bf(v[i] + rv[i]);
+      if (bi < rows_m) st_out(&y[size_t(m0 + bi) * p.ldy + col], o);
+      sq[i] = bi < rows_m ? bf2f(o) * bf2f(o) : 0.f;
+    }
+    if (p.ss_out) {
+      // the next RMSNorm's statistics: sum of squares of this warp's 32
+      // output columns per batch row, one partial per (tile, TMEM quadrant)
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) sq[i] += __shfl_xor_sync(0xffffffffu, sq[i], off);
+      if (lane < 16 && 16 * j + lane < rows_m) {
+        float mine = sq[0];
+#pragma unroll
+        for (int i = 1; i < 16; ++i) if (lane == i) mine = sq[i];
+        p.ss_out[size_t(out_col0 / 32 + q) * p.M + m0 + 16 * j + lane] = mine;
+      }
     }
   }
 }
@@ -1647,6 +1665,19 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
   const int cw = ct >> 5;                 // consumer warp index (amx slot)
   const int half = ct >> 7;               // which column groups (j parity)
   const int chunks = p.K / p.T_K;
+  if (p.ss_in) {
+    // RMSNorm folded into the weights (W * gamma): 1/rms of every batch row
+    // from the producer's per-tile partial sums of squares -- one round trip
+    // while the MMAs of the first segment run
+    const int b = ct >> 2, sub = ct & 3;
+    float t = 0.f;
+    if (b < p.M)
+      for (int k = sub; k < p.ss_nparts; k += 4) t += __ldcg(p.ss_in + size_t(k) * p.M + b);
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    t += __shfl_xor_sync(0xffffffffu, t, 2);
+    if (sub == 0 && b < kAmaxRows) s.rsn[b] = rsqrtf(t / float(p.K) + p.norm_eps);
+    bar_sync(1, kCons);
+  }
   SegIter it;
   it.init(p, a.W, w_in_task);
   Seg g;
@@ -1668,6 +1699,10 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
         float rv[16], v[16];
         umma_res16(p, m0, rows_m, out_col0 + row, j, rv);
         tmem_acc16(s.tmem_base, q, buf, j, v);
+        if (p.ss_in) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] *= s.rsn[(m0 + 16 * j + i) & (kAmaxRows - 1)];
+        }
         umma_epi16(a, s, p, m0, rows_m, out_col0, row, q, lane, cw, j, v, rv);
       }
       tc_fence_before();
@@ -1736,6 +1771,10 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
         for (int u = 0; u < 3; ++u)
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] += t[u][i];
+      }
+      if (p.ss_in) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] *= s.rsn[(m0 + 16 * j + i) & (kAmaxRows - 1)];
       }
       umma_epi16(a, s, p, m0, rows_m, out_col0, row, q, lane, cw, j, v, rv);
     }
@@ -1894,6 +1933,19 @@ __device__ void run_rmsnorm(const KArgs& a, Smem& s, const mk_task& t, int ib, i
 #pragma unroll
           for (int i = 0; i < kRegChunks; ++i)
             if (lane * 8 + i * 256 < p.d) *reinterpret_cast<uint4*>(xs + lane * 8 + i * 256) = xv[i];
+        }
+        if (p.ss_out) {         // the folded-norm consumer's statistics (one partial)
+          float ss = 0.f;
+#pragma unroll
+          for (int i = 0; i < kRegChunks; ++i) {
+            float f[8];
+            unpack8(xv[i], f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) ss = fmaf(f[e], f[e], ss);
+          }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+          if (lane == 0) p.ss_out[b] = ss;
         }
         continue;
       }
@@ -3604,7 +3656,8 @@ static int validate_graph(const mk_graph_desc* g) {
       if (p->body == MK_BODY_UMMA) {
         const int R = p->T_N * (p->epilogue == MK_EPI_SILU ? 2 : 1);
         if (R != 128 || p->T_K != 64 || p->K % 64 || p->N % 128 || p->T_M > 64 || p->stage_x ||
-            p->norm_gamma || (p->epilogue == MK_EPI_LOGITS && p->M > kAmaxRows))
+            p->norm_gamma || (p->epilogue == MK_EPI_LOGITS && p->M > kAmaxRows) ||
+            (p->ss_in && (p->ss_nparts < 1 || p->M > kAmaxRows)))
           return fail(MK_ERR_CONFIG, "umma gemm task " + std::to_string(i) + " has an unsupported tile");
         continue;
       }

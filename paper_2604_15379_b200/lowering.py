@@ -263,8 +263,12 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
 
     def gemm_params(w, x, y, res, M, K, N, tile, ldx, ldy, ldres, col0, epi,
                     xcd, tm=-1, tn=-1, amax_base=0, gamma=None, y_cols=None,
-                    ksplit=False):
+                    ksplit=False, ss_in=None, ss_out=None):
         p = L.GemmParams()
+        if ss_in is not None:          # RMSNorm folded into these weights
+            p.ss_in, p.ss_nparts = _ptr(ss_in[0]), ss_in[1]
+            p.norm_eps = spec.eps
+        p.ss_out = _ptr(ss_out)
         umma = is_umma_tile(tile, epi == L.EPI_SILU)
         rows = tile[1] * (2 if epi == L.EPI_SILU else 1)
         if ksplit and not ksplit_pays(_cdiv(M, tile[0]) * (N // rows), opts.workers):
@@ -295,9 +299,10 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         p.amax_base, p.amax_stride = amax_base, B
         return blob.add(p)
 
-    def norm_params(layer_bufs, x, gamma, y, embed=False, fused=False):
+    def norm_params(layer_bufs, x, gamma, y, embed=False, fused=False, ss_out=None):
         p = L.NormParams()
         p.fused = 1 if fused else 0
+        p.ss_out = _ptr(ss_out)
         p.x, p.gamma, p.y = _ptr(x), _ptr(gamma), _ptr(y)
         if embed:
             p.embed = _ptr(bufs.embed)
@@ -355,7 +360,11 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
     fused_reduce = (attn_mma and opts.fuse_attn_reduce
                     and int(os.environ.get("MK_ATTN_WPI", "1")) == 1)
     ksplit = opts.ksplit and per_die and bufs.kpart is not None
-    fuse = opts.fuse_norm and all(
+    # tcgen05 graphs: each RMSNorm folded into its consumer's weights
+    # (runtime.build_state packs W * gamma); the residual-producing GEMMs
+    # emit per-tile sums of squares, the consumer scales by 1/rms
+    fold = (opts.fuse_norm and getattr(bufs, "fold_norm", False) and opts.tp_world == 1)
+    fuse = not fold and opts.fuse_norm and all(
         stages(B, d, tl) and not is_umma_tile(tl, f)
         for tl, f in ((gemm_tile_of(OpKind.QKV_PROJ), False),
                       (gemm_tile_of(OpKind.GATE_UP_SILU), gu_fused),
@@ -412,13 +421,14 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
             if first:
                 src = bufs.x_in0 if layer == 0 else bufs.layers[layer - 1]["x_out"]
                 po = norm_params(lb, src, wl["in_norm"], lb["normed1"],
-                                 embed=(layer == 0), fused=fuse)
+                                 embed=(layer == 0), fused=fuse or fold,
+                                 ss_out=bufs.ss_in0 if (fold and layer == 0) else None)
             else:
                 po = norm_params(lb, lb["x_mid"], wl["post_norm"], lb["normed2"],
-                                 fused=fuse)
+                                 fused=fuse or fold)
             add_task(t.id, gi, L.OP_RMSNORM, level, None, wait, t.signal_event,
                      po, layer, n_items=B, n_units=u_rows)
-            if fuse and opts.bypass_noop and not (first and layer == 0) and wait:
+            if (fuse or fold) and opts.bypass_noop and not (first and layer == 0) and wait:
                 bypass[t.signal_event] = wait
         elif op in (OpKind.QKV_PROJ, OpKind.O_PROJ_RESIDUAL,
                     OpKind.GATE_UP_SILU, OpKind.DOWN_PROJ_RESIDUAL):
@@ -433,22 +443,32 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
             tile = tuple(t.tile_shape)
             x_in = bufs.x_in0 if layer == 0 else bufs.layers[layer - 1]["x_out"]
             gamma = None
+            ss_in = ss_out = None
+            n_parts = d // 32
             if op is OpKind.QKV_PROJ:
                 w, x, y, res, epi, ldx, ldy = (bufs.w_packed[layer]["qkv"],
                                               lb["normed1"], lb["qkv_out"], None,
                                               L.EPI_NONE, d, spec.qkv_dim)
                 if fuse:
                     x, gamma = x_in, wl["in_norm"]
+                if fold:
+                    x = x_in
+                    ss_in = (bufs.ss_in0, 1) if layer == 0 else \
+                        (bufs.layers[layer - 1]["ss_out"], n_parts)
             elif op is OpKind.O_PROJ_RESIDUAL:
                 w, x, y, res, epi, ldx, ldy = (bufs.w_packed[layer]["o"],
                                               lb["attn_out"], lb["x_mid"], x_in,
                                               L.EPI_RESIDUAL, K, d)
+                if fold:
+                    ss_out = lb["ss_mid"]
             elif op is OpKind.GATE_UP_SILU:
                 fused = t.level is TaskLevel.CHIPLET
                 w = bufs.w_packed[layer]["gate_up"]
                 x, ldx = lb["normed2"], d
                 if fuse:
                     x, gamma = lb["x_mid"], wl["post_norm"]
+                if fold:
+                    x, ss_in = lb["x_mid"], (lb["ss_mid"], n_parts)
                 if fused:
                     y, epi, ldy = lb["silu_out"], L.EPI_SILU, F
                 else:
@@ -458,6 +478,8 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                 w, x, y, res, epi, ldx, ldy = (bufs.w_packed[layer]["down"],
                                               lb["silu_out"], lb["x_out"],
                                               lb["x_mid"], L.EPI_RESIDUAL, F, d)
+                if fold:
+                    ss_out = lb["ss_out"]
             ar = None
             if tp and op in (OpKind.O_PROJ_RESIDUAL, OpKind.DOWN_PROJ_RESIDUAL):
                 # row-parallel: the fp32 partial goes to every rank (y is this
@@ -473,14 +495,16 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                 col0 = xd * (n_loc // 2 if epi == L.EPI_SILU else n_loc)
                 po = gemm_params(_ptr(w, xd * n_loc * K), _ptr(x), _ptr(y),
                                  _ptr(res), M, K, n_loc, tile, ldx, ldy, d,
-                                 col0, epi, xd, gamma=gamma, ksplit=ksplit)
+                                 col0, epi, xd, gamma=gamma, ksplit=ksplit,
+                                 ss_in=ss_in, ss_out=ss_out)
                 add_task(t.id, gi, L.OP_GEMM, level, xd, wait, t.signal_event,
                          po, layer, n_items=0)
             else:
                 work = t.work
                 po = gemm_params(_ptr(w), _ptr(x), _ptr(y), _ptr(res), M, K, N,
                                  tile, ldx, ldy, d, 0, epi, 0,
-                                 tm=work.m_idx, tn=work.n_idx, gamma=gamma)
+                                 tm=work.m_idx, tn=work.n_idx, gamma=gamma,
+                                 ss_in=ss_in, ss_out=ss_out)
                 add_task(t.id, gi, L.OP_GEMM, level, None, wait, t.signal_event,
                          po, layer)
             if ar is not None and gi == last_of[(t.id.split(".")[0], op)]:
@@ -528,12 +552,13 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         event_names.append(e)
         required.append(0)
     x_last = bufs.layers[n_layers - 1]["x_out"]
-    po = norm_params(None, x_last, bufs.final_norm, bufs.final_normed, fused=fuse)
-    lm_x = x_last if fuse else bufs.final_normed
+    po = norm_params(None, x_last, bufs.final_norm, bufs.final_normed, fused=fuse or fold)
+    lm_x = x_last if (fuse or fold) else bufs.final_normed
     lm_gamma = bufs.final_norm if fuse else None
+    lm_ss = (bufs.layers[n_layers - 1]["ss_out"], d // 32) if fold else None
     add_task("final_norm.t0", -1, L.OP_RMSNORM, L.LEVEL_CU, None, last_event,
              "e.final_norm", po, n_layers, n_items=B, n_units=u_rows)
-    lm_wait = last_event if (fuse and opts.bypass_noop) else "e.final_norm"
+    lm_wait = last_event if ((fuse or fold) and opts.bypass_noop) else "e.final_norm"
     required[ev_index["e.final_norm"]] = 1
     t_m, t_n, t_k = opts.lm_tile
     V = bufs.vocab_pad or spec.vocab          # padded for 128-row tcgen05 tiles
@@ -547,7 +572,7 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                              B, d, n_loc, (t_m, t_n, t_k), d, V, d,
                              xd * n_loc, L.EPI_LOGITS, xd,
                              amax_base=xd * opts.workers, gamma=lm_gamma,
-                             y_cols=spec.vocab, ksplit=ksplit)
+                             y_cols=spec.vocab, ksplit=ksplit, ss_in=lm_ss)
             add_task(f"lm_head.x{xd}", -1, L.OP_GEMM, L.LEVEL_CHIPLET, xd,
                      lm_wait, "e.lm_head", po, n_layers, n_items=0)
         required[ev_index["e.lm_head"]] = X
@@ -559,7 +584,8 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
                 po = gemm_params(_ptr(bufs.lm_packed), _ptr(lm_x),
                                  _ptr(logits), None, B, d, V, (t_m, t_n, t_k),
                                  d, V, d, 0, L.EPI_LOGITS, 0, tm=m, tn=n,
-                                 amax_base=n, gamma=lm_gamma, y_cols=spec.vocab)
+                                 amax_base=n, gamma=lm_gamma, y_cols=spec.vocab,
+                                 ss_in=lm_ss)
                 add_task(f"lm_head.t{m * nt + n}", -1, L.OP_GEMM, L.LEVEL_CU,
                          None, lm_wait, "e.lm_head", po, n_layers)
         required[ev_index["e.lm_head"]] = mt * nt

@@ -118,11 +118,14 @@ class DeviceState:
     rope_sin: torch.Tensor = None
     vocab_pad: int = 0
     page_table: torch.Tensor = None
+    fold_norm: bool = False
+    ss_in0: torch.Tensor = None
 
 
 def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
                 amax_slots: int, device="cuda", split: int | None = None,
-                keep_logits: bool = True, kv_pages: int | None = None) -> DeviceState:
+                keep_logits: bool = True, kv_pages: int | None = None,
+                allow_fold: bool = True) -> DeviceState:
     """Device buffers of one lowered graph.  ``kv_pages``: paged KV -- every
     layer's K and V become pools of ``kv_pages`` pages of ``split`` tokens
     ([pages][kv_heads][split][head_dim]) addressed through a per-row page
@@ -139,6 +142,17 @@ def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
     w = weights.to(dev)
     tiles = _graph_tiles(g)
     chiplet = g.mode == "chiplet"
+    # tcgen05 everywhere: RMSNorms are folded into their consumers' weights
+    # (W * gamma, packed below); lowering.lower scales by 1/rms in the
+    # epilogue from the sums of squares the residual GEMMs emit
+    fold = (allow_fold and os.environ.get("MK_NO_FOLD") is None
+            and all(is_umma_tile(tiles[op], op is OpKind.GATE_UP_SILU and chiplet)
+                for op in (OpKind.QKV_PROJ, OpKind.O_PROJ_RESIDUAL,
+                           OpKind.GATE_UP_SILU, OpKind.DOWN_PROJ_RESIDUAL))
+            and is_umma_tile(lm_tile, False))
+    st.fold_norm = fold
+    fl = (lambda w_, gam: (w_.float() * gam.float()[None, :]).to(w_.dtype)) if fold \
+        else (lambda w_, gam: w_)
     X = g.machine.num_xcds
     bf = dict(device=dev, dtype=torch.bfloat16)
     # layers from the graph's stages (a reference-built TaskGraph carries no
@@ -152,16 +166,19 @@ def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
             _, tn, tk = tiles[op]
             return pack_umma(w_, tn, tk) if is_umma_tile(tiles[op], False) else pack_tiles(w_, tn, tk)
 
-        packed = {"qkv": pk(qkv, OpKind.QKV_PROJ), "o": pk(Lw["o"], OpKind.O_PROJ_RESIDUAL),
+        packed = {"qkv": pk(fl(qkv, Lw["in_norm"]), OpKind.QKV_PROJ),
+                  "o": pk(Lw["o"], OpKind.O_PROJ_RESIDUAL),
                   "down": pk(Lw["down"], OpKind.DOWN_PROJ_RESIDUAL)}
         gt = tiles[OpKind.GATE_UP_SILU]
         if chiplet:
             if is_umma_tile(gt, True):
-                packed["gate_up"] = pack_gate_up_umma(Lw["gate"], Lw["up"], X, gt[2])
+                packed["gate_up"] = pack_gate_up_umma(fl(Lw["gate"], Lw["post_norm"]),
+                                                      fl(Lw["up"], Lw["post_norm"]), X, gt[2])
             else:
                 packed["gate_up"] = pack_gate_up_fused(Lw["gate"], Lw["up"], X, gt[1], gt[2])
         else:
-            packed["gate_up"] = pk(torch.cat((Lw["gate"], Lw["up"]), 0), OpKind.GATE_UP_SILU)
+            packed["gate_up"] = pk(fl(torch.cat((Lw["gate"], Lw["up"]), 0), Lw["post_norm"]),
+                                   OpKind.GATE_UP_SILU)
         st.w_packed.append(packed)
         st.w_layers.append({k: Lw[k] for k in ("q_norm", "k_norm", "in_norm", "post_norm")})
         st.layers.append({
@@ -173,6 +190,9 @@ def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
             "gu_out": torch.zeros(B, 2 * sp.ffn, **bf) if not chiplet else None,
             "silu_out": torch.zeros(B, sp.ffn, **bf),
             "x_out": torch.zeros(B, sp.hidden, **bf),
+            # folded-norm statistics: per (32-column group) sums of squares
+            "ss_mid": torch.zeros(sp.hidden // 32, B, device=dev) if fold else None,
+            "ss_out": torch.zeros(sp.hidden // 32, B, device=dev) if fold else None,
         })
         kv_shape = (kv_pages, sp.kv_heads, split, hd) if kv_pages else (B, sp.kv_heads, t_max, hd)
         st.k_cache.append(torch.zeros(*kv_shape, **bf))
@@ -181,13 +201,14 @@ def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
     _, tn, tk = lm_tile
     if is_umma_tile(lm_tile, False):
         st.vocab_pad = -(-sp.vocab // 256) * 256          # 128-row tiles per die
-        st.lm_packed = pack_umma(pad_rows(w.lm_head, 256), tn, tk)
+        st.lm_packed = pack_umma(pad_rows(fl(w.lm_head, w.final_norm), 256), tn, tk)
     else:
         st.vocab_pad = sp.vocab
         st.lm_packed = pack_tiles(w.lm_head, tn, tk)
     st.embed = w.embed
     st.final_norm = w.final_norm
     st.x_in0 = torch.zeros(B, sp.hidden, **bf)
+    st.ss_in0 = torch.zeros(1, B, device=dev) if fold else None
     st.final_normed = torch.zeros(B, sp.hidden, **bf)
     st.logits = torch.zeros(B, st.vocab_pad, device=dev, dtype=torch.float32) \
         if keep_logits else None
@@ -280,7 +301,8 @@ class Megakernel:
         amax_slots = (n_dies * workers) if per_die else v_pad // lm_tile[1]
         self.state = build_state(g, weights, t_max, lm_tile, amax_slots,
                                  device=f"cuda:{device}",
-                                 keep_logits=keep_logits, kv_pages=kv_pages)
+                                 keep_logits=keep_logits, kv_pages=kv_pages,
+                                 allow_fold=self.tp[1] == 1)
         self.pool = PagePool(kv_pages) if kv_pages else None
         if self.pool:
             self._table = torch.full((g.batch, self.state.n_splits), -1, dtype=torch.int32)

@@ -1,7 +1,9 @@
 """Summarise an ncu report (raw page) into markdown: duration, DRAM bytes and
 throughput, L2 hit rate, tensor-pipe activity, top stall reasons.
 
-    python tools/ncu_summary.py <report.ncu-rep> "<title>" > profiles/rNN/x.md
+    python tools/ncu_summary.py <report.ncu-rep | raw.csv> "<title>" > profiles/rNN/x.md
+
+(a raw.csv is the `ncu -i rep --page raw --csv` export of the report)
 """
 import csv
 import io
@@ -22,8 +24,11 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 def main():
     rep = sys.argv[1]
     title = sys.argv[2] if len(sys.argv) > 2 else rep
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
-                         capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
+                             capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     out = [f"# ncu summary: {title}", "", f"report: `{rep}`", "",
