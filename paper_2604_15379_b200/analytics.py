@@ -95,7 +95,7 @@ def fit_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
 
 
 # batch rows from which the tcgen05 body is used (MK_UMMA_MIN_BATCH overrides)
-UMMA_MIN_BATCH = int(os.environ.get("MK_UMMA_MIN_BATCH", "4"))
+UMMA_MIN_BATCH = int(os.environ.get("MK_UMMA_MIN_BATCH", "3"))
 UMMA_MAX_TM = 64         # batch rows per tcgen05 m-tile (UMMA N, TMEM columns)
 
 

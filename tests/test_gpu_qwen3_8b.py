@@ -196,9 +196,10 @@ def test_qwen3_8b_widths_decode_matches_oracle(topo, machine, w2, B):
                 low.params[t.param_off:t.param_off + ctypes.sizeof(L.AttnParams)])
             attn.add((p.mma, p.sub_splits, p.fuse_reduce, p.group, p.n_splits))
     # the configuration the bench runs at this batch
-    assert bodies == ({L.BODY_GEMV} if B < 4 else {L.BODY_UMMA})
+    from paper_2604_15379_b200.analytics import UMMA_MIN_BATCH
+    assert bodies == ({L.BODY_GEMV} if B < UMMA_MIN_BATCH else {L.BODY_UMMA})
     assert attn == {(1, 1, 0, 4, 18)} and mk.kv_swizzled
-    if B >= 4:
+    if B >= UMMA_MIN_BATCH:
         assert mk.state.vocab_pad == 152064 and ksplit > 0
     ref = Qwen3Fp32(cpu, t_max=1152, batch=B)
     _context(mk, ref, B, seed=40 + B)
