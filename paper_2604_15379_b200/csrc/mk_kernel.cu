@@ -2308,9 +2308,11 @@ __device__ __forceinline__ uint32_t kv_swz(int token, int chunk) {   // byte off
   return uint32_t(token * (kAttnHD * 2) + ((chunk ^ (token & 7)) << 4));
 }
 
+constexpr int kQRows = 8;                       // rows whose q a unit pre-rotates
 struct AttnMmaScratch {
   uint16_t q[kConsWarps][kAttnMaxG][kAttnHD];  // per warp: normed + roped q of the group
   float xch[kConsWarps][kAttnMaxG][kAttnHD + 4];  // per warp: (o[128], m, l) per head
+  uint16_t qrow[kQRows][kAttnMaxG][kAttnHD];   // per unit: normed + roped q of its rows
 };
 static_assert(sizeof(AttnMmaScratch) <= size_t(kXsBytes), "attention scratch exceeds the union");
 
@@ -2337,16 +2339,20 @@ __device__ __forceinline__ void attn_mma_tokens(const KArgs& a, Smem& s, uint8_t
                                                 int nvalid, int tok0, int tpw, uint32_t kpos,
                                                 bool tagged, int warp, int lane,
                                                 float (&o)[16][4], float& m_run, float& l_run,
-                                                bool trace, uint64_t& ph1, uint64_t& ph2) {
+                                                bool trace, uint64_t& ph1, uint64_t& ph2,
+                                                const uint16_t* qpre = nullptr) {
   const int G = p.group;
   const int g = lane >> 2, c = lane & 3;
   AttnMmaScratch& sc = *reinterpret_cast<AttnMmaScratch*>(s.u.xs);
+  // q of the item's row: pre-rotated once per unit (qpre, [G][128]) or
+  // normed + roped here into the warp's scratch
+  const uint16_t* qs = qpre ? qpre : &sc.q[warp][0][0];
     const uint16_t* qkv = reinterpret_cast<const uint16_t*>(p.qkv) + size_t(b) * p.ldqkv;
     const float* cs = p.rope_cos + size_t(pos) * (kAttnHD / 2);
     const float* sn = p.rope_sin + size_t(pos) * (kAttnHD / 2);
     const int dl = lane & 15, half = lane >> 4;
     // q_norm + RoPE of the item's G heads -> bf16 (unscaled, as the model's q)
-    for (int h = half; h < G; h += 2) {
+    for (int h = half; h < G && !qpre; h += 2) {
       float qv[8];
       norm_rope8<kAttnHD>(qkv + (p.kv_head * G + h) * kAttnHD, reinterpret_cast<const uint16_t*>(p.q_gamma),
                           p.eps, cs, sn, dl, qv);
@@ -2386,8 +2392,8 @@ __device__ __forceinline__ void attn_mma_tokens(const KArgs& a, Smem& s, uint8_t
     uint32_t qa0[8], qa2[8];
 #pragma unroll
     for (int st = 0; st < 8; ++st) {
-      qa0[st] = g < G ? *reinterpret_cast<const uint32_t*>(&sc.q[warp][g][16 * st + 2 * c]) : 0u;
-      qa2[st] = g < G ? *reinterpret_cast<const uint32_t*>(&sc.q[warp][g][16 * st + 8 + 2 * c]) : 0u;
+      qa0[st] = g < G ? *reinterpret_cast<const uint32_t*>(qs + g * kAttnHD + 16 * st + 2 * c) : 0u;
+      qa2[st] = g < G ? *reinterpret_cast<const uint32_t*>(qs + g * kAttnHD + 16 * st + 8 + 2 * c) : 0u;
     }
     const uint32_t ks = smem_u32(kslot), vs = smem_u32(vslot);
     const float qscale = p.scale * 1.4426950408889634f;
@@ -2612,6 +2618,36 @@ __device__ void attn_mma_free(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
   uint32_t act = 0;                          // active items before the current one
   int last_b = -1, pos = 0;
   const bool trace = a.log != nullptr && lane == 0 && warp == 0;
+  // q_norm + RoPE of every row of the unit once (each row's q is shared by
+  // all its splits): the per-item path then starts from shared memory
+  // instead of an L2 round trip per item
+  AttnMmaScratch& sc = *reinterpret_cast<AttnMmaScratch*>(s.u.xs);
+  const int r0 = ib < ie ? ib / p.n_splits : 0;
+  int nq = ib < ie ? min(kQRows, (ie - 1) / p.n_splits - r0 + 1) : 0;
+  if (ie - ib > kConsWarps) {                // worth it: more items than warps
+    const int dl = lane & 15, half = lane >> 4;
+    for (int task = warp; task < nq * ((G + 1) / 2); task += kConsWarps) {
+      const int rr = task / ((G + 1) / 2), h = 2 * (task % ((G + 1) / 2)) + half;
+      const int bq = r0 + rr;
+      int pq = row_pos(p.positions, bq);
+      if (pq < 0 || pq >= p.t_max) pq = 0;     // reported by the item loop (pos_ok)
+      if (h < G) {
+        float qv[8];
+        norm_rope8<kAttnHD>(reinterpret_cast<const uint16_t*>(p.qkv) + size_t(bq) * p.ldqkv +
+                                (p.kv_head * G + h) * kAttnHD,
+                            reinterpret_cast<const uint16_t*>(p.q_gamma), p.eps,
+                            p.rope_cos + size_t(pq) * (kAttnHD / 2),
+                            p.rope_sin + size_t(pq) * (kAttnHD / 2), dl, qv);
+        uint4 pk;
+        pk.x = pack_bf16(qv[0], qv[1]); pk.y = pack_bf16(qv[2], qv[3]);
+        pk.z = pack_bf16(qv[4], qv[5]); pk.w = pack_bf16(qv[6], qv[7]);
+        *reinterpret_cast<uint4*>(&sc.qrow[rr][h][dl * 8]) = pk;
+      }
+    }
+    bar_sync(1, kCons);
+  } else {
+    nq = 0;
+  }
   for (int it = ib; it < ie; ++it) {
     const int b = it / p.n_splits, sp = it % p.n_splits;
     if (b != last_b) {
@@ -2635,7 +2671,8 @@ __device__ void attn_mma_free(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
     const int nvalid = min(kAttnSplit, pos + 1 - t0);
     const bool stamp = a.trace != nullptr && ct == 0 && s.tr[3] == 0;
     attn_mma_tokens(a, s, ring, p, b, pos, t0, nvalid, 0, kAttnSplit, kpos, true, warp, lane,
-                    o, m_run, l_run, trace || stamp, ph1, ph2);
+                    o, m_run, l_run, trace || stamp, ph1, ph2,
+                    b - r0 < nq ? &sc.qrow[b - r0][0][0] : nullptr);
     if (stamp) { s.tr[7] = ph1; s.tr[3] = ph2; }   // q norm+RoPE done / K,V slots ready
     __syncwarp();
     if (lane == 0) {
