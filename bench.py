@@ -162,7 +162,8 @@ def build(args, device):
         lm_tile = _default_lm_tile(spec, args.batch, args.t_m)
     mk = Megakernel(g, w, t_max=t_max, traversal=trav, distribution=distn, sched=sched,
                     topo=topo, keep_logits=False, device=device, lm_tile=lm_tile,
-                    ksplit=not args.no_ksplit)
+                    ksplit=not args.no_ksplit,
+                    fuse_attn_reduce=os.environ.get("MK_FUSE_ATTN_REDUCE") == "1")
     del w
     torch.cuda.empty_cache()
     mk.fill_kv_random(CTX)
