@@ -55,8 +55,8 @@ constexpr int kProdThreads = 128;              // producer warpgroup (warp 0 fet
 constexpr int kThreads = kCons + kProdThreads;  // 12 warps = 3 warpgroups
 constexpr int kProdRegs = 88;                   // setmaxnreg budget: 128*88 + 256*200
 constexpr int kConsRegs = 200;                  //   = 62464 <= 65536
-constexpr int kProdRegsUmma = 152;              // tcgen05 instance: 128*152 + 256*176
-constexpr int kConsRegsUmma = 176;              //   = 64512 <= 65536
+constexpr int kProdRegsUmma = 104;              // tcgen05 instance: 128*104 + 256*200
+constexpr int kConsRegsUmma = 200;              //   = 64512 = the 168 x 384 the launch holds
 constexpr int kSlotBytes = 16384;
 constexpr int kSlots = 10;
 constexpr int kXsBytes = 49152;                 // staged activations per task / x ring
