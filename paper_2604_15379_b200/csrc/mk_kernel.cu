@@ -133,8 +133,8 @@ struct KArgs {
   int debug;               // bit0: consumers skip GEMM math, bit1: fetch issues no TMA
   int use_umma;            // graph has tcgen05 GEMM tasks: allocate TMEM, run the MMA warp
   const CUtensorMap* tmaps; // [n_tasks]: activation (x) tensor map of each tcgen05 GEMM task
-  int x_stages;            // x ring stages (kXsBytes / x_stage_bytes, <= kXStagesMax)
-  int x_stage_bytes;       // 128 * max NT over the graph's tcgen05 tasks
+  int x_stages;            // x ring stages of two chunks (kXsBytes / (2 x_stage_bytes))
+  int x_stage_bytes;       // one chunk: 128 * max NT over the graph's tcgen05 tasks
   int pf_slots;            // L2 prefetch run-ahead of the prefetch warp (16 KiB slots)
   const int32_t* positions; // decode position per row (read once per launch into smem)
   int n_rows;
@@ -1419,15 +1419,19 @@ __device__ void xload_warp(const KArgs& a, Smem& s) {
     Seg g;
     while (lt.next(g)) {
       const int row = g.m * p.T_M;
-      for (int c = g.c0; c < g.c1; ++c) {
+      // one stage = the activation chunks of one MMA chunk pair (the MMA
+      // warp pairs c0, c0+1, ... of each segment; a last odd chunk alone)
+      for (int c = g.c0; c < g.c1; c += 2) {
+        const int n = min(2, g.c1 - c);
         if (!mbar_spin(a, &s.xempty[xl], xph ^ 1, -13)) return;
         if (leader) {
           if (no_tma) {                // diagnostics: no activation TMA
             mbar_arrive(&s.xfull[xl]);
           } else {
-            mbar_arrive_expect_tx(&s.xfull[xl], x_bytes);
-            tma_load_2d(reinterpret_cast<uint8_t*>(s.u.xs) + size_t(xl) * XB, tmap, c * 64, row,
-                        &s.xfull[xl]);
+            uint8_t* dst = reinterpret_cast<uint8_t*>(s.u.xs) + size_t(xl) * 2 * XB;
+            mbar_arrive_expect_tx(&s.xfull[xl], uint32_t(n) * x_bytes);
+            tma_load_2d(dst, tmap, c * 64, row, &s.xfull[xl]);
+            if (n == 2) tma_load_2d(dst + XB, tmap, (c + 1) * 64, row, &s.xfull[xl]);
           }
         }
         __syncwarp();
@@ -1481,55 +1485,45 @@ __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
       tc_fence_after();
       const uint32_t d = tmem0 + uint32_t(buf * kBufCols);
       int c = sg.c0;
-      // chunk pairs: one loop pass (waits, fences, issue setup) per 32 KiB
-      for (; !no_mma && c + 1 < sg.c1; c += 2) {
+      // chunk pairs: one loop pass (waits, fences, issue setup) per 32 KiB;
+      // the pair's activation chunks share one x stage (xload_warp pairs
+      // the segment's chunks the same way; a last odd chunk has its own)
+      for (; c < sg.c1; c += 2) {
+        const bool pair = c + 1 < sg.c1;
         const int ri1 = ri + 1 == kSlots ? 0 : ri + 1;
         const uint32_t rph1 = ri + 1 == kSlots ? rph ^ 1 : rph;
-        const int xi1 = xi + 1 == XS ? 0 : xi + 1;
-        const uint32_t xph1 = xi + 1 == XS ? xph ^ 1 : xph;
         if (prof) {
-          n_chunks += 2;
+          n_chunks += pair ? 2 : 1;
           ok = mbar_wait_p(a, &s.full[ri], rph, -11, w_full) && mbar_wait_p(a, &s.xfull[xi], xph, -12, w_x) &&
-               mbar_wait_p(a, &s.full[ri1], rph1, -11, w_full) && mbar_wait_p(a, &s.xfull[xi1], xph1, -12, w_x);
+               (!pair || mbar_wait_p(a, &s.full[ri1], rph1, -11, w_full));
         } else {
           ok = mbar_spin(a, &s.full[ri], rph, -11) && mbar_spin(a, &s.xfull[xi], xph, -12) &&
-               mbar_spin(a, &s.full[ri1], rph1, -11) && mbar_spin(a, &s.xfull[xi1], xph1, -12);
+               (!pair || mbar_spin(a, &s.full[ri1], rph1, -11));
         }
         if (!__all_sync(0xffffffffu, ok)) return;
         tc_fence_after();
-        umma_chunk8(d, adesc0 + uint64_t(ri * (kSlotBytes >> 4)), bdesc0 + uint64_t(xi * (XB >> 4)),
-                    adesc0 + uint64_t(ri1 * (kSlotBytes >> 4)), bdesc0 + uint64_t(xi1 * (XB >> 4)),
-                    idesc, c != sg.c0 ? 1u : 0u, &s.empty[ri], &s.empty[ri1], kConsWarps - 1,
-                    &s.xempty[xi], &s.xempty[xi1]);
-        __syncwarp();
-        ri = ri1 + 1 == kSlots ? 0 : ri1 + 1;
-        rph = ri1 + 1 == kSlots ? rph1 ^ 1 : rph1;
-        xi = xi1 + 1 == XS ? 0 : xi1 + 1;
-        xph = xi1 + 1 == XS ? xph1 ^ 1 : xph1;
-      }
-      for (; c < sg.c1; ++c) {
-        if (prof) ++n_chunks;
-        if (prof) {
-          ok = mbar_wait_p(a, &s.full[ri], rph, -11, w_full) && mbar_wait_p(a, &s.xfull[xi], xph, -12, w_x);
-        } else {
-          ok = mbar_spin(a, &s.full[ri], rph, -11) && mbar_spin(a, &s.xfull[xi], xph, -12);
-        }
-        if (!__all_sync(0xffffffffu, ok)) return;
-        tc_fence_after();
+        const uint64_t bx = bdesc0 + uint64_t(xi * (2 * XB >> 4));   // the stage of this pair
         if (no_mma) {                    // diagnostics: no MMA, release at once
           if (leader) {
             mbar_arrive_cnt(&s.empty[ri], kConsWarps);
+            if (pair) mbar_arrive_cnt(&s.empty[ri1], kConsWarps);
             mbar_arrive(&s.xempty[xi]);
           }
+        } else if (pair) {
+          umma_chunk8(d, adesc0 + uint64_t(ri * (kSlotBytes >> 4)), bx,
+                      adesc0 + uint64_t(ri1 * (kSlotBytes >> 4)), bx + uint64_t(XB >> 4),
+                      idesc, c != sg.c0 ? 1u : 0u, &s.empty[ri], &s.empty[ri1], kConsWarps - 1,
+                      &s.xempty[xi]);
         } else {
           // UMMA_K = 16 bf16 = 32 B along the swizzled row, 4 per 64-wide chunk;
           // ring slot: 8 arrivals (one per GEMV consumer warp), 7 plain, the
           // eighth from the commit when the MMAs have read the slot
-          umma_chunk4(d, adesc0 + uint64_t(ri * (kSlotBytes >> 4)), bdesc0 + uint64_t(xi * (XB >> 4)),
+          umma_chunk4(d, adesc0 + uint64_t(ri * (kSlotBytes >> 4)), bx,
                       idesc, c != sg.c0 ? 1u : 0u, &s.empty[ri], kConsWarps - 1, &s.xempty[xi]);
         }
         __syncwarp();
-        if (++ri == kSlots) { ri = 0; rph ^= 1; }
+        if (pair) { ri = ri1 + 1 == kSlots ? 0 : ri1 + 1; rph = ri1 + 1 == kSlots ? rph1 ^ 1 : rph1; }
+        else { ri = ri1; rph = rph1; }
         if (++xi == XS) { xi = 0; xph ^= 1; }
       }
       if (leader) {
@@ -3780,7 +3774,8 @@ static int build_tmaps(mk_handle* h, const mk_graph_desc* g) {
   }
   h->x_stage_bytes = max_nt * 128;
   int xs = 1;                                       // as many stages as fit
-  xs = std::max(1, std::min(kXStagesMax, kXsBytes / h->x_stage_bytes));
+  // one stage holds the activation chunks of one MMA chunk pair
+  xs = std::max(1, std::min(kXStagesMax, kXsBytes / (2 * h->x_stage_bytes)));
   h->x_stages = xs;
   if (any) {
     CK(cudaMalloc(&h->d_tmaps, maps.size() * sizeof(CUtensorMap)));

@@ -315,12 +315,12 @@ __device__ __forceinline__ void umma_chunk4(uint32_t d_tmem, uint64_t a0, uint64
       : "memory");
 }
 
-// Two K-chunks in one block (8 MMAs): chunk 0 on (a0, b0) releasing
-// slot0 / x0, chunk 1 on (a1, b1) releasing slot1 / x1.
+// Two K-chunks in one block (8 MMAs): chunk 0 on (a0, b0) releasing slot0,
+// chunk 1 on (a1, b1) releasing slot1, then the pair's activation stage x.
 __device__ __forceinline__ void umma_chunk8(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint64_t a1,
                                             uint64_t b1, uint32_t idesc, uint32_t accumulate,
                                             uint64_t* slot0, uint64_t* slot1, uint32_t arrivals,
-                                            uint64_t* x0, uint64_t* x1) {
+                                            uint64_t* x) {
   asm volatile(
       "{\n\t.reg .pred e, p, t;\n\t"
       ".reg .b64 c1, c2, c3, d1, d2, d3, f1, f2, f3, g1, g2, g3;\n\t"
@@ -339,17 +339,15 @@ __device__ __forceinline__ void umma_chunk8(uint32_t d_tmem, uint64_t a0, uint64
       "@e tcgen05.mma.cta_group::1.kind::f16 [e3], c3, d3, %5, p;\n\t"
       "@e mbarrier.arrive.shared::cta.b64 _, [%7], %9;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%7];\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %4, %5, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [e1], f1, g1, %5, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [e2], f2, g2, %5, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f16 [e3], f3, g3, %5, t;\n\t"
       "@e mbarrier.arrive.shared::cta.b64 _, [%8], %9;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%11];\n\t}"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%10];\n\t}"
       :: "r"(d_tmem), "l"(a0), "l"(b0), "l"(a1), "l"(b1), "r"(idesc), "r"(accumulate),
-         "r"(smem_u32(slot0)), "r"(smem_u32(slot1)), "r"(arrivals), "r"(smem_u32(x0)),
-         "r"(smem_u32(x1))
+         "r"(smem_u32(slot0)), "r"(smem_u32(slot1)), "r"(arrivals), "r"(smem_u32(x))
       : "memory");
 }
 
