@@ -215,9 +215,8 @@ def run_ours(args):
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        mk.state.tokens.copy_(h_tok, non_blocking=True)
-        mk.launch()
-        h_out.copy_(mk.state.out_tokens, non_blocking=True)
+        # the C-ABI call with host buffers: H2D tokens, launch, D2H greedy ids
+        mk.launch_host(h_tok, h_out, stream)
         e1.record(stream)
         e1.synchronize()
         h_tok.copy_(h_out)

@@ -266,6 +266,9 @@ typedef struct mk_graph_desc {
                                 read once per launch (borrowed)               */
   int32_t n_rows;
   int32_t pad;
+  int32_t* tokens;           /* device [n_rows]: token ids this step decodes
+                                (borrowed; written by mk_step_tokens)        */
+  const int32_t* out_tokens; /* device [n_rows]: greedy ids the step emits     */
 } mk_graph_desc;
 
 typedef struct mk_counters {
@@ -311,6 +314,11 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo,
 /* One decode step (one cooperative launch) on `stream` (cudaStream_t, may be
  * NULL).  Asynchronous: check mk_sync() for the watchdog verdict. */
 int mk_step(mk_handle* h, void* stream);
+/* One decode step with host token buffers: copies
+ * `tokens_in` [n_rows] host->device, launches, copies the greedy ids
+ * device->host into `tokens_out`, all on `stream`; completes at mk_sync /
+ * stream synchronisation (pinned host memory for true asynchrony). */
+int mk_step_tokens(mk_handle* h, void* stream, const int32_t* tokens_in, int32_t* tokens_out);
 int mk_sync(mk_handle* h);
 int mk_counters_get(mk_handle* h, mk_counters* out);
 int mk_counters_reset(mk_handle* h);

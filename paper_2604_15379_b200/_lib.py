@@ -100,7 +100,7 @@ class GraphDesc(C.Structure):
                 ("workers_per_sched", I32), ("param_bytes", I32),
                 ("tasks", P), ("event_required", P), ("units", P),
                 ("sched_begin", P), ("params", P), ("positions", P), ("n_rows", I32),
-                ("pad", I32)]
+                ("pad", I32), ("tokens", P), ("out_tokens", P)]
 
 
 class Counters(C.Structure):
@@ -120,7 +120,8 @@ class LogRec(C.Structure):
                 ("t_start", C.c_uint64), ("t_end", C.c_uint64)]
 
 
-EXPORTS = ("mk_probe", "mk_probe_raw", "mk_create", "mk_step", "mk_sync", "mk_counters_get",
+EXPORTS = ("mk_probe", "mk_probe_raw", "mk_create", "mk_step", "mk_step_tokens", "mk_sync",
+           "mk_counters_get",
            "mk_counters_reset", "mk_log_enable", "mk_log_read",
            "mk_tile_log_enable", "mk_tile_log_read", "mk_trace_enable", "mk_trace_read",
            "mk_set_watchdog", "mk_set_prefetch", "mk_set_debug",
@@ -145,6 +146,7 @@ def load() -> C.CDLL:
     lib.mk_create.argtypes = [C.c_int, C.POINTER(GraphDesc), C.POINTER(Topology),
                               C.POINTER(C.c_void_p)]
     lib.mk_step.argtypes = [C.c_void_p, C.c_void_p]
+    lib.mk_step_tokens.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.mk_set_prefetch.argtypes = [C.c_void_p, C.c_int]
     lib.mk_sync.argtypes = [C.c_void_p]
     lib.mk_counters_get.argtypes = [C.c_void_p, C.POINTER(Counters)]

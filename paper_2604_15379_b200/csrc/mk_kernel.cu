@@ -3493,6 +3493,8 @@ struct mk_handle {
   int tp_world = 1, tp_rank = 0;
   uint8_t* tp_peer[MK_MAX_TP] = {};
   bool has_tp_tasks = false;
+  int32_t* tokens = nullptr;
+  const int32_t* out_tokens = nullptr;
 };
 
 static const void* kernel_for(int feat) {
@@ -3819,6 +3821,8 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
   h->n_units = g->n_units;
   h->n_sub = g->n_sub_ctrs;
   h->positions = g->positions;
+  h->tokens = g->tokens;
+  h->out_tokens = g->out_tokens;
   h->n_rows = g->positions ? g->n_rows : 0;
   std::vector<int8_t> die_of_sm(MK_MAX_SMS, 0);
   h->group_size.assign(MK_MAX_DIES, 0);
@@ -3965,6 +3969,20 @@ int mk_step(mk_handle* h, void* stream) {
                         kSmemBytes, static_cast<cudaStream_t>(stream)));
   }
   h->epoch = a.epoch;
+  return MK_OK;
+}
+
+int mk_step_tokens(mk_handle* h, void* stream, const int32_t* tokens_in, int32_t* tokens_out) {
+  if (!h) return fail(MK_ERR_CONFIG, "null handle");
+  if (!h->tokens || !h->out_tokens)
+    return fail(MK_ERR_CONFIG, "graph descriptor carries no token buffers");
+  CK(cudaSetDevice(h->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t bytes = sizeof(int32_t) * size_t(h->n_rows);
+  if (tokens_in) CK(cudaMemcpyAsync(h->tokens, tokens_in, bytes, cudaMemcpyHostToDevice, st));
+  const int rc = mk_step(h, stream);
+  if (rc != MK_OK) return rc;
+  if (tokens_out) CK(cudaMemcpyAsync(tokens_out, h->out_tokens, bytes, cudaMemcpyDeviceToHost, st));
   return MK_OK;
 }
 

@@ -153,6 +153,8 @@ class Lowered:
     kv_swizzled: bool = False      # KV rows chunk-swizzled (tensor-core attention)
     positions: int = 0             # device pointer of the per-row decode positions
     n_rows: int = 0
+    tokens: int = 0                # device pointers of the step's token ids / greedy ids
+    out_tokens: int = 0
     keep: list = field(default_factory=list)   # ctypes arrays kept alive
 
     def desc(self) -> L.GraphDesc:
@@ -174,6 +176,8 @@ class Lowered:
         g.params = C.cast(pbuf, C.c_void_p)
         g.positions = self.positions
         g.n_rows = self.n_rows
+        g.tokens = self.tokens
+        g.out_tokens = self.out_tokens
         return g
 
 
@@ -624,7 +628,8 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
     return Lowered(t_arr, u_arr, b_arr, r_arr, bytes(blob.data), event_names,
                    names, gidx, n_sub[0], n_sched, opts.sched_mode,
                    opts.workers, amax_slots, kv_swizzled=attn_mma,
-                   positions=_ptr(bufs.positions) or 0, n_rows=B)
+                   positions=_ptr(bufs.positions) or 0, n_rows=B,
+                   tokens=_ptr(bufs.tokens) or 0, out_tokens=_ptr(bufs.out_tokens) or 0)
 
 
 def _silu_meta(g: TaskGraph, B: int, F: int):

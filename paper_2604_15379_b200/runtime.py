@@ -471,6 +471,26 @@ class Megakernel:
         self._pos += 1                          # the argmax task advances the positions
         self.steps += 1
 
+    def launch_host(self, tokens_in, tokens_out, stream=None):
+        """One step through mk_step_tokens: ``tokens_in`` / ``tokens_out`` are
+        host int32 tensors [B] (pinned for asynchrony); the copies and the
+        launch are queued on ``stream``."""
+        if int(self._pos.max()) >= self.state.t_max:
+            raise L.MkError(L.MK_ERR_CONFIG, f"decode position {int(self._pos.max())} "
+                            f"reached t_max={self.state.t_max}")
+        for t in (tokens_in, tokens_out):
+            if t is not None and (t.device.type != "cpu" or t.dtype != torch.int32
+                                  or t.numel() != self.graph.batch):
+                raise ValueError("host int32 tensors of batch size expected")
+        self._ensure_pages(self._pos)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        L.check(self.lib.mk_step_tokens(
+            self.h, C.c_void_p(s.cuda_stream),
+            C.c_void_p(tokens_in.data_ptr() if tokens_in is not None else 0),
+            C.c_void_p(tokens_out.data_ptr() if tokens_out is not None else 0)))
+        self._pos += 1
+        self.steps += 1
+
     def sync(self):
         L.check(self.lib.mk_sync(self.h))
 

@@ -483,3 +483,26 @@ def test_run_is_a_simulate_dropin_with_reference_records(topo, machine):
     assert "L2Hit% standard" in table and "HBMRd xstandard chiplet" in table
     c = report.compare(traces["standard"], traces["chiplet"]).to_json()
     assert c["baseline_mode"] == "standard" and c["ratios"]["dispatches"] > 0
+
+
+def test_step_with_host_token_buffers(topo, machine):
+    """mk_step_tokens: host token ids in, host greedy ids out,
+    copies and launch on one stream -- the same tokens as the device-buffer
+    path, equal to the argmax of the step's logits."""
+    from paper_2604_15379_b200.runtime import Megakernel
+    from paper_2604_15379_b200.weights import Qwen3Spec, Qwen3Weights
+    w = Qwen3Weights.random(Qwen3Spec.toy(), seed=17)
+    g = _toy_graph(machine, "chiplet", 3)
+    a = Megakernel(g, w, t_max=32, topo=topo)
+    b = Megakernel(g, w, t_max=32, topo=topo)
+    h_in = torch.tensor([5, 77, 300], dtype=torch.int32).pin_memory()
+    h_out = torch.zeros(3, dtype=torch.int32).pin_memory()
+    for _ in range(4):
+        a.launch_host(h_in, h_out)
+        a.sync()
+        want = b.step(h_in.clone()).cpu()
+        assert h_out.tolist() == want.tolist() == a.logits().float().argmax(-1).cpu().tolist()
+        h_in.copy_(h_out)
+    assert a.positions().tolist() == [4, 4, 4]
+    a.close()
+    b.close()
