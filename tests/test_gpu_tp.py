@@ -114,3 +114,57 @@ def test_tp2_qwen3_8b_widths_on_one_gpu_matches_oracle(topo):
     _decode(mks, ref, 1, steps=3, seed=7)
     for mk in mks:
         mk.close()
+
+
+def _ipc_child(handle, nbytes, q):
+    import ctypes as C
+    import torch as T
+    from paper_2604_15379_b200 import _lib as L
+    lib = L.load()
+    T.cuda.set_device(0)
+    buf = (C.c_uint8 * 64).from_buffer_copy(handle)
+    ptr = C.c_void_p()
+    L.check(lib.mk_ipc_import(0, buf, C.byref(ptr)))
+    # read the parent's pattern through the imported mapping, then write back
+    n = nbytes // 4
+    # wrap the raw device pointer with a torch tensor via __cuda_array_interface__
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr.value, False),
+                                    "version": 3}
+    peer = T.as_tensor(_Arr(), device="cuda")
+    ok = bool(T.equal(peer, T.arange(n, device="cuda", dtype=T.int32)))
+    peer.mul_(2)
+    T.cuda.synchronize()
+    L.check(lib.mk_ipc_close(ptr))
+    q.put(ok)
+
+
+def test_exchange_region_ipc_between_processes():
+    """dist.connect_dist's plumbing: an exchange region from mk_tp_alloc,
+    exported with mk_ipc_export, opened by another process with
+    mk_ipc_import -- both see the same device memory."""
+    import ctypes as C
+    import torch.multiprocessing as mp
+    from paper_2604_15379_b200 import _lib as L
+    lib = L.load()
+    n = 1 << 16
+    ptr = C.c_void_p()
+    L.check(lib.mk_tp_alloc(0, 4 * n, C.byref(ptr)))
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<i4", "data": (ptr.value, False),
+                                    "version": 3}
+    mine = torch.as_tensor(_Arr(), device="cuda")
+    mine.copy_(torch.arange(n, device="cuda", dtype=torch.int32))
+    torch.cuda.synchronize()
+    h = (C.c_uint8 * 64)()
+    L.check(lib.mk_ipc_export(ptr, h))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_ipc_child, args=(bytes(h), 4 * n, q))
+    p.start()
+    ok = q.get(timeout=120)
+    p.join(timeout=60)
+    assert ok and p.exitcode == 0
+    assert torch.equal(mine, 2 * torch.arange(n, device="cuda", dtype=torch.int32))
+    L.check(lib.mk_tp_free(ptr))
