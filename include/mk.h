@@ -213,7 +213,11 @@ typedef struct mk_attn_params {
                           k_cache / v_cache are then page pools
                           [n_pages][kv_heads][split][head_dim]            */
   int32_t max_pages;   /* pages per row (t_max / split)                     */
-  int32_t pad;
+  int32_t prefill;     /* 1: chunked prefill -- the M rows are consecutive
+                          tokens of ONE sequence (positions p0..p0+M-1, the
+                          same pages): every item also folds the chunk's
+                          earlier tokens into its K/V slots (tensor-core
+                          path, M <= 64)                                   */
 } mk_attn_params;
 
 typedef struct mk_silu_params {

@@ -74,7 +74,7 @@ class AttnParams(C.Structure):
                 ("split", I32), ("n_splits", I32), ("t_max", I32),
                 ("eps", F32), ("scale", F32), ("sub_splits", I32), ("mma", I32),
                 ("fuse_reduce", I32), ("red_ctr0", I32), ("page_table", P),
-                ("max_pages", I32), ("pad", I32)]
+                ("max_pages", I32), ("prefill", I32)]
 
 
 class SiluParams(C.Structure):

@@ -207,6 +207,7 @@ constexpr size_t kRingOffset = (sizeof(Smem) + 1023) / 1024 * 1024;
 constexpr int kAttnHD = 128;
 constexpr int kAttnSplit = 64;
 constexpr int kAttnMaxG = 4;                   // query heads per kv head on this path
+constexpr int kChunkRows = 64;                  // chunked prefill: tokens per launch
 
 __host__ __device__ __forceinline__ bool attn_mma_path(const mk_attn_params& p) {
   return p.mma != 0 && p.head_dim == kAttnHD && p.split == kAttnSplit && p.group <= kAttnMaxG;
@@ -2305,8 +2306,14 @@ __device__ __forceinline__ uint32_t kv_swz(int token, int chunk) {   // byte off
 constexpr int kQRows = 8;                       // rows whose q a unit pre-rotates
 struct AttnMmaScratch {
   uint16_t q[kConsWarps][kAttnMaxG][kAttnHD];  // per warp: normed + roped q of the group
-  float xch[kConsWarps][kAttnMaxG][kAttnHD + 4];  // per warp: (o[128], m, l) per head
   uint16_t qrow[kQRows][kAttnMaxG][kAttnHD];   // per unit: normed + roped q of its rows
+  union {
+    float xch[kConsWarps][kAttnMaxG][kAttnHD + 4];  // pass variant: (o[128], m, l) per head
+    struct {                                        // chunked prefill: the chunk's
+      uint16_t k[kChunkRows][kAttnHD];              //   normed + roped k rows
+      uint16_t v[kChunkRows][kAttnHD];              //   and v rows (this kv head)
+    } ch;
+  };
 };
 static_assert(sizeof(AttnMmaScratch) <= size_t(kXsBytes), "attention scratch exceeds the union");
 
@@ -2380,6 +2387,19 @@ __device__ __forceinline__ void attn_mma_tokens(const KArgs& a, Smem& s, uint8_t
       const size_t crow = kv_off(p, b, pos);
       uint16_t* cache = reinterpret_cast<uint16_t*>(half == 0 ? p.k_cache : p.v_cache);
       *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(cache + crow) + ((dl ^ (pos & 7)) << 4)) = kv4;
+    }
+    if (p.prefill) {
+      // chunked prefill: the chunk's earlier tokens (other rows of this
+      // launch, appended concurrently) come from the unit's staged rows, not
+      // from the cache the slots were loaded from
+      const int p0 = row_pos(p.positions, 0);
+      const int lo = max(t0 + tok0, p0), hi = min(pos - 1, t0 + tok0 + tpw - 1);
+      for (int P = lo + (lane >> 4); P <= hi; P += 2) {
+        const int r = P - p0;
+        const uint32_t off = kv_swz(P - t0, dl);
+        *reinterpret_cast<uint4*>(kslot + off) = *reinterpret_cast<const uint4*>(&sc.ch.k[r][dl * 8]);
+        *reinterpret_cast<uint4*>(vslot + off) = *reinterpret_cast<const uint4*>(&sc.ch.v[r][dl * 8]);
+      }
     }
     __syncwarp();
     // Q fragments: row g = head g (g < G), 8 k-steps of 16 dims
@@ -2641,6 +2661,31 @@ __device__ void attn_mma_free(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
     bar_sync(1, kCons);
   } else {
     nq = 0;
+  }
+  if (p.prefill && ib < ie) {
+    // chunked prefill: k_norm + RoPE and v of every chunk row (this kv head)
+    // into shared memory once per unit; items fold them into their slots
+    const int dl = lane & 15, half = lane >> 4;
+    for (int rr = warp; rr < p.M && rr < kChunkRows; rr += kConsWarps) {
+      int pq = row_pos(p.positions, rr);
+      if (pq < 0 || pq >= p.t_max) pq = 0;
+      const uint16_t* row = reinterpret_cast<const uint16_t*>(p.qkv) + size_t(rr) * p.ldqkv;
+      float kn[8];                 // both half-warps (norm_rope8 shuffles within halves)
+      norm_rope8<kAttnHD>(row + p.q_heads * kAttnHD + p.kv_head * kAttnHD,
+                          reinterpret_cast<const uint16_t*>(p.k_gamma), p.eps,
+                          p.rope_cos + size_t(pq) * (kAttnHD / 2),
+                          p.rope_sin + size_t(pq) * (kAttnHD / 2), dl, kn);
+      if (half == 0) {
+        uint4 k4;
+        k4.x = pack_bf16(kn[0], kn[1]); k4.y = pack_bf16(kn[2], kn[3]);
+        k4.z = pack_bf16(kn[4], kn[5]); k4.w = pack_bf16(kn[6], kn[7]);
+        *reinterpret_cast<uint4*>(&sc.ch.k[rr][dl * 8]) = k4;
+      } else {
+        *reinterpret_cast<uint4*>(&sc.ch.v[rr][dl * 8]) =
+            ldg128_cg(row + (p.q_heads + p.kv_heads) * kAttnHD + p.kv_head * kAttnHD + dl * 8);
+      }
+    }
+    bar_sync(1, kCons);
   }
   for (int it = ib; it < ie; ++it) {
     const int b = it / p.n_splits, sp = it % p.n_splits;
@@ -3718,7 +3763,8 @@ static int validate_graph(const mk_graph_desc* g) {
       if ((hd != 16 && hd != 32 && hd != 64 && hd != 128) || p->group < 1 || p->group > 8 ||
           8 % p->group || size_t(p->split) * hd * 2 > size_t(kSlotBytes) ||
           p->n_splits > kMaxSplits || p->sub_splits < 1 || !ws_ok || (mma && p->t_max % kAttnSplit) ||
-          (p->page_table && p->max_pages * p->split != p->t_max))
+          (p->page_table && p->max_pages * p->split != p->t_max) ||
+          (p->prefill && (!mma || p->M > kChunkRows || p->sub_splits != 1)))
         return fail(MK_ERR_CONFIG, "attention task " + std::to_string(i) + " has unsupported shapes");
     }
   }

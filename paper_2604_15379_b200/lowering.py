@@ -89,6 +89,9 @@ class LoweringOptions:
                                    # measured slower (one warp merges serially)
     ksplit: bool = True            # die tasks: K-split slot ranges per worker
                                    # instead of whole tiles
+    prefill: bool = False          # chunked prefill: the rows are consecutive
+                                   # tokens of one sequence (attention folds the
+                                   # chunk's earlier tokens into its slots)
     tp_rank: int = 0               # tensor parallelism: this
     tp_world: int = 1              # rank of the group; spec / buffers are the
     tp_layout: object = None       # rank's shard (runtime.build_state), TPLayout
@@ -333,6 +336,10 @@ def lower(g: TaskGraph, spec, bufs, opts: LoweringOptions) -> Lowered:
         if getattr(bufs, "page_table", None) is not None:       # paged KV pools
             p.page_table = _ptr(bufs.page_table)
             p.max_pages = bufs.page_table.shape[1]
+        if opts.prefill:
+            if not attn_mma:
+                raise ValueError("chunked prefill needs the tensor-core attention path")
+            p.prefill = 1
         p.out = _ptr(out)
         p.M, p.ldqkv = B, spec.qkv_dim
         p.q_heads, p.kv_heads, p.head_dim = spec.q_heads, spec.kv_heads, hd

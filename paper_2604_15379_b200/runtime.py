@@ -125,7 +125,7 @@ class DeviceState:
 def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
                 amax_slots: int, device="cuda", split: int | None = None,
                 keep_logits: bool = True, kv_pages: int | None = None,
-                allow_fold: bool = True) -> DeviceState:
+                allow_fold: bool = True, kv_share: "DeviceState | None" = None) -> DeviceState:
     """Device buffers of one lowered graph.  ``kv_pages``: paged KV -- every
     layer's K and V become pools of ``kv_pages`` pages of ``split`` tokens
     ([pages][kv_heads][split][head_dim]) addressed through a per-row page
@@ -195,8 +195,12 @@ def build_state(g: TaskGraph, weights: Qwen3Weights, t_max: int, lm_tile,
             "ss_out": torch.zeros(sp.hidden // 32, B, device=dev) if fold else None,
         })
         kv_shape = (kv_pages, sp.kv_heads, split, hd) if kv_pages else (B, sp.kv_heads, t_max, hd)
-        st.k_cache.append(torch.zeros(*kv_shape, **bf))
-        st.v_cache.append(torch.zeros(*kv_shape, **bf))
+        if kv_share is not None:        # another instance's page pools (chunked prefill)
+            st.k_cache.append(kv_share.k_cache[li])
+            st.v_cache.append(kv_share.v_cache[li])
+        else:
+            st.k_cache.append(torch.zeros(*kv_shape, **bf))
+            st.v_cache.append(torch.zeros(*kv_shape, **bf))
     del w.layers[:]
     _, tn, tk = lm_tile
     if is_umma_tile(lm_tile, False):
@@ -255,7 +259,8 @@ class Megakernel:
                  keep_logits: bool = True, watchdog_s: float = 10.0,
                  ksplit: bool = True, fuse_attn_reduce: bool = False,
                  tp: tuple | None = None, ctas: int | None = None,
-                 cooperative: bool = True, kv_pages: int | None = None):
+                 cooperative: bool = True, kv_pages: int | None = None,
+                 prefill_for: "Megakernel | None" = None):
         """``tp=(rank, world)``: this rank's shard of a Megatron tensor-
         parallel group (``weights`` are the full model; dist.shard_weights
         slices them); join the group with dist.connect_local /
@@ -264,7 +269,10 @@ class Megakernel:
         on disjoint SMs (``cooperative=False``: plain launches).
         ``kv_pages``: paged KV cache with a pool of that many pages of one
         attention split (64 tokens on the tensor-core path) per layer; pages
-        are assigned as rows advance and returned by release_row()."""
+        are assigned as rows advance and returned by release_row().
+        ``prefill_for=mk``: a chunked-prefill instance for the paged decode
+        instance ``mk`` (same weights, same page pools): its B rows are B
+        consecutive prompt tokens of one of mk's sequences (mk.prefill_chunked)."""
         if not torch.cuda.is_available():
             raise RuntimeError("Megakernel needs a CUDA device (no CPU fallback)")
         self.lib = L.load()
@@ -295,15 +303,23 @@ class Megakernel:
             sched_mode=L.SCHED_PER_DIE if per_die else L.SCHED_FLAT,
             traversal=traversal, distribution=distribution, workers=workers,
             n_dies=n_dies, fanout=fanout, lm_tile=lm_tile,
-            fuse_attn_reduce=fuse_attn_reduce)
+            fuse_attn_reduce=fuse_attn_reduce, prefill=prefill_for is not None)
         v_pad = (-(-self.spec.vocab // 256) * 256) if is_umma_tile(lm_tile, False) \
             else self.spec.vocab
         amax_slots = (n_dies * workers) if per_die else v_pad // lm_tile[1]
+        if prefill_for is not None:
+            if not prefill_for.pool or prefill_for.state.t_max != t_max:
+                raise ValueError("chunked prefill needs a paged decode instance with the same t_max")
+            kv_pages = prefill_for.pool.n_pages
         self.state = build_state(g, weights, t_max, lm_tile, amax_slots,
                                  device=f"cuda:{device}",
                                  keep_logits=keep_logits, kv_pages=kv_pages,
-                                 allow_fold=self.tp[1] == 1)
-        self.pool = PagePool(kv_pages) if kv_pages else None
+                                 allow_fold=self.tp[1] == 1,
+                                 kv_share=prefill_for.state if prefill_for is not None else None)
+        self.prefill_for = prefill_for
+        # a prefill instance's page table rows all point at the sequence being
+        # prefilled (set per chunk); it allocates nothing itself
+        self.pool = PagePool(kv_pages) if (kv_pages and prefill_for is None) else None
         if self.pool:
             self._table = torch.full((g.batch, self.state.n_splits), -1, dtype=torch.int32)
         if per_die and ksplit:
@@ -527,6 +543,38 @@ class Megakernel:
                 if t >= lens[b] - 1 and len(outs[b]) < max_new_tokens:
                     outs[b].append(prev[b])
         return outs
+
+    def prefill_chunked(self, row: int, prompt, pf: "Megakernel"):
+        """Chunked device prefill of sequence ``row``: ``pf`` (an instance
+        built with ``prefill_for=self``) decodes pf.batch prompt tokens per
+        launch -- its rows are consecutive positions of this one sequence,
+        sharing its pages; the KV of the whole prompt lands in this
+        instance's page pools.  Afterwards row ``row`` continues at position
+        len(prompt); returns the greedy token after the prompt."""
+        if pf.prefill_for is not self:
+            raise ValueError("pf was not built with prefill_for=self")
+        T, C_ = len(prompt), pf.graph.batch
+        if T < 1 or T > self.state.t_max:
+            raise ValueError("prompt length out of range")
+        self.release_row(row)
+        self._ensure_pages([T - 1 if b == row else 0 for b in range(self.graph.batch)])
+        table = self.state.page_table[row].clone()
+        pf.state.page_table.copy_(table.expand(C_, -1))
+        nxt = None
+        for c0 in range(0, T, C_):
+            n = min(C_, T - c0)
+            # pad rows repeat the last real token at its position (identical
+            # K/V writes); their outputs are ignored
+            pos = [c0 + min(r, n - 1) for r in range(C_)]
+            toks = [prompt[c0 + min(r, n - 1)] for r in range(C_)]
+            pf._pos = torch.tensor(pos, dtype=torch.int64)
+            pf.state.positions.copy_(pf._pos.to(torch.int32))
+            out = pf.step(toks).cpu().tolist()
+            nxt = out[n - 1]
+        self._pos[row] = T
+        self.state.positions[row] = T
+        self._ensure_pages(self._pos)
+        return nxt
 
     def prefill(self, prompts):
         """Build every row's KV context from its prompt on the device;
