@@ -935,7 +935,7 @@ __device__ void gemm_tile_fast(const KArgs& a, Smem& s, uint8_t* ring, Ring& r,
                                float (&amv)[NB], int (&ami)[NB]) {
   constexpr int NP = 4 / RPW;
   constexpr int KC = 256 * NP;
-  constexpr int CH = (RPW * NB >= 4) ? 1 : NP;   // extra chains when few (row, b) pairs
+  constexpr int CH = (RPW * NB > 4) ? 1 : NP;    // extra chains when few (row, b) pairs
   const int warp = ct >> 5, lane = ct & 31;
   const int chunks = p.K / KC;
   const int m0 = m * p.T_M;
@@ -1074,7 +1074,7 @@ __device__ __forceinline__ void gemm_tile_fast_ks(const KArgs& a, Smem& s, uint8
   Ring rl = r;                             // keep the ring cursor in a register
   constexpr int NP = 4 / RPW;
   constexpr int KC = 256 * NP;
-  constexpr int CH = (RPW * NB >= 4) ? 1 : NP;   // extra chains when few (row, b) pairs
+  constexpr int CH = (RPW * NB > 4) ? 1 : NP;    // extra chains when few (row, b) pairs
   const int warp = ct >> 5, lane = ct & 31;
   const int chunks = p.K / KC;
   const int m0 = m * p.T_M;

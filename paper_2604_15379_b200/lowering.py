@@ -134,7 +134,7 @@ class TPLayout:
     def nbytes(self) -> int:
         return self.gather_off + self.world * self.batch * 8
 
-XS_BYTES = 32768                   # kXsBytes in mk_kernel.cu
+XS_BYTES = 49152                   # kXsBytes in mk_kernel.cu
 PIECE_FLOATS = 128 * 64            # K-split piece: 128 weight rows x 64 batch rows
 
 
