@@ -1412,9 +1412,26 @@ __device__ void xload_warp(const KArgs& a, Smem& s) {
     const mk_gemm_params& p = *P<mk_gemm_params>(a, s.tcache[job.w]);
     const void* tmap = a.tmaps + job.x;
     const uint32_t x_bytes = uint32_t(umma_nt(p)) * 128u;
-    // the consumers acquired the job's input event: order those generic
-    // writes before the async-proxy (TMA) reads of x
-    if (leader) fence_proxy_async_global();
+    // the job arrives before its dependency resolved: acquire the unit's
+    // input events here (relaxed polls + one acquire fence), then order the
+    // producers' generic writes before the async-proxy (TMA) reads of x
+    {
+      const mk_task& t = s.tcache[job.w];
+      bool ok = true;
+      if (leader) {
+        for (int k = 0; k < 2 && ok; ++k) {
+          const int e = k ? t.wait1 : t.wait0;
+          if (e < 0) continue;
+          const uint32_t target = uint32_t(t.pad[k]) * a.epoch;
+          Spin sp;
+          while ((int32_t)(ld_relaxed(&a.ev_ctr[e]) - target) < 0)
+            if (!sp.ok(a, -15)) { ok = false; break; }
+        }
+        fence_acq_rel_gpu();
+        fence_proxy_async_global();
+      }
+      if (!__shfl_sync(0xffffffffu, ok ? 1 : 0, 0)) return;
+    }
     SegIter lt;
     lt.init(p, a.W, job.y);
     Seg g;
@@ -1455,6 +1472,9 @@ __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
   unsigned long long w_full = 0, w_x = 0, w_tmem = 0, n_chunks = 0;
   // diagnostics flags read once: the per-chunk path paces the die task
   const bool prof = (a.debug & 4) != 0, no_mma = (a.debug & 8) != 0;
+  // trace diagnostics (debug bit 5): stamps 6/7 = first operands ready / last commit
+  const bool stamp = a.trace != nullptr && (a.debug & 32) != 0;
+  const int dbg_mode = (a.debug & 64) ? 1 : (a.debug & 128) ? 2 : 0;   // umma_chunk8_dbg
   const uint64_t adesc0 = umma_desc_sw128(smem_u32(ring));
   const uint64_t bdesc0 = umma_desc_sw128(smem_u32(s.u.xs));
   for (;;) {
@@ -1475,6 +1495,7 @@ __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
     SegIter it;
     it.init(p, a.W, job.y);
     Seg sg;
+    bool first_pair = true;
     for (;;) {
       if (!__shfl_sync(0xffffffffu, it.next(sg) ? 1 : 0, 0)) break;
       sg.c0 = __shfl_sync(0xffffffffu, sg.c0, 0);
@@ -1502,6 +1523,8 @@ __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
                (!pair || mbar_spin(a, &s.full[ri1], rph1, -11));
         }
         if (!__all_sync(0xffffffffu, ok)) return;
+        if (stamp && first_pair && leader) s.tr[6] = globaltimer();   // first pair's operands ready
+        first_pair = false;
         tc_fence_after();
         const uint64_t bx = bdesc0 + uint64_t(xi * (2 * XB >> 4));   // the stage of this pair
         if (no_mma) {                    // diagnostics: no MMA, release at once
@@ -1510,6 +1533,11 @@ __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
             if (pair) mbar_arrive_cnt(&s.empty[ri1], kConsWarps);
             mbar_arrive(&s.xempty[xi]);
           }
+        } else if (pair && dbg_mode) {
+          umma_chunk8_dbg(dbg_mode, d, adesc0 + uint64_t(ri * (kSlotBytes >> 4)), bx,
+                          adesc0 + uint64_t(ri1 * (kSlotBytes >> 4)), bx + uint64_t(XB >> 4),
+                          idesc, c != sg.c0 ? 1u : 0u, &s.empty[ri], &s.empty[ri1], kConsWarps - 1,
+                          &s.xempty[xi]);
         } else if (pair) {
           umma_chunk8(d, adesc0 + uint64_t(ri * (kSlotBytes >> 4)), bx,
                       adesc0 + uint64_t(ri1 * (kSlotBytes >> 4)), bx + uint64_t(XB >> 4),
@@ -1534,6 +1562,7 @@ __device__ void mma_warp(const KArgs& a, Smem& s, uint8_t* ring) {
       __syncwarp();
       ++tb_k;
     }
+    if (stamp && leader) s.tr[7] = globaltimer();                  // the job's last commit issued
   }
   if (leader && prof) {
     atomicAdd(&a.stats[S_W_MMA_FULL], w_full); atomicAdd(&a.stats[S_W_MMA_X], w_x);
@@ -1715,6 +1744,7 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
     // (first_w, first_w+1, ...: deterministic, arrival-order independent).
     const PieceInfo pi = tile_pieces(p, a.W, g.tile);
     if (w_in_task != pi.first_w) {
+      if ((a.debug & 256) && a.trace && ct == 0) s.tr[6] = globaltimer();   // accumulator ready
       float* mine = piece_ptr(p, w_in_task, g.first ? 0 : 1);
       for (int j = half; j < NT / 16; j += 2) {
         float v[16];
@@ -1729,6 +1759,7 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
       ++tb_k;
       bar_sync(2, kCons);
       if (ct == 0) {                        // cumulative release of the CTA's stores
+        if ((a.debug & 256) && a.trace) s.tr[7] = globaltimer();     // pieces stored, CTA joined
         fence_acq_rel_gpu();
         red_release_add(&a.sub_ctr[p.tile_ctr0 + g.tile], 1u);
       }
@@ -1739,12 +1770,12 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
     // operands and up to three pieces in flight together, own partial from
     // TMEM, sum in piece order, epilogue; the accumulator is released last
     if (ct == 0) {
-      if (a.trace) s.tr[7] = globaltimer();          // own accumulator ready
+      if (a.trace && !(a.debug & 288)) s.tr[7] = globaltimer();  // own accumulator ready
       const uint32_t target = uint32_t(pi.n - 1) * a.epoch;
       Spin sp;
       while ((int32_t)(ld_acquire(&a.sub_ctr[p.tile_ctr0 + g.tile]) - target) < 0)
         if (!sp.ok(a, -18)) break;
-      if (a.trace) s.tr[6] = globaltimer();          // the other pieces arrived
+      if (a.trace && !(a.debug & 288)) s.tr[6] = globaltimer();  // the other pieces arrived
     }
     bar_sync(2, kCons);
     for (int j = half; j < NT / 16; j += 2) {
@@ -1811,10 +1842,7 @@ __device__ void run_gemm_umma(const KArgs& a, Smem& s, Ring& r, const mk_task& t
     }
   }
   bar_sync(1, kCons);
-  if (ct == 0) {
-    s.job = make_int4(tix, w_in_task, int(r.k), int(&t - s.tcache));
-    mbar_arrive(&s.job_full);
-  }
+  (void)tix;                        // the job was posted at dequeue (consumers())
   MK_TRACE(a, s, ct, 3);
   umma_epilogue(a, s, p, w_in_task, ct, tb_k);
   (void)xs_k;
@@ -3232,6 +3260,17 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
 #pragma unroll
           for (int i = 0; i < 8; ++i) s.tr[i] = 0;
           s.tr[1] = globaltimer();
+        }
+        if constexpr ((F & kFeatUmma) != 0) {
+          // tcgen05 GEMM: hand the job to the x-load / MMA warps BEFORE the
+          // dependency resolves; the x-load warp acquires the input event
+          // itself and issues the activation TMA at once, so the first MMA
+          // is not serialised behind this role's acquire + code fetch
+          // (the previous job was consumed: its accumulator was drained)
+          if (t.op == MK_OP_GEMM && P<mk_gemm_params>(a, t)->body == MK_BODY_UMMA) {
+            s.job = make_int4(ent.x, t.level == MK_LEVEL_CHIPLET ? worker : 0, int(r.k), qi);
+            mbar_arrive(&s.job_full);
+          }
         }
         for (int k = 0; k < 2; ++k) {
           const int e = waits[k];

@@ -351,6 +351,52 @@ __device__ __forceinline__ void umma_chunk8(uint32_t d_tmem, uint64_t a0, uint64
       : "memory");
 }
 
+// Diagnostics variants of umma_chunk8 (timing only; results are wrong):
+// mode 1: one commit per pair (slot0 and x released by plain arrivals);
+// mode 2: only the first chunk's 4 MMAs, commits as umma_chunk8.
+__device__ __forceinline__ void umma_chunk8_dbg(int mode, uint32_t d_tmem, uint64_t a0, uint64_t b0,
+                                                uint64_t a1, uint64_t b1, uint32_t idesc,
+                                                uint32_t accumulate, uint64_t* slot0, uint64_t* slot1,
+                                                uint32_t arrivals, uint64_t* x) {
+  if (mode == 1) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t"
+        ".reg .b64 c1, c2, c3, d1, d2, d3, f1, f2, f3, g1, g2, g3;\n\t"
+        ".reg .b32 e1, e2, e3, n1;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "setp.eq.b32 t, 0, 0;\n\t"
+        "add.u32 e1, %0, 64; add.u32 e2, %0, 128; add.u32 e3, %0, 192; add.u32 n1, %9, 1;\n\t"
+        "add.s64 c1, %1, 2; add.s64 c2, %1, 4; add.s64 c3, %1, 6;\n\t"
+        "add.s64 d1, %2, 2; add.s64 d2, %2, 4; add.s64 d3, %2, 6;\n\t"
+        "add.s64 f1, %3, 2; add.s64 f2, %3, 4; add.s64 f3, %3, 6;\n\t"
+        "add.s64 g1, %4, 2; add.s64 g2, %4, 4; add.s64 g3, %4, 6;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [e1], c1, d1, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [e2], c2, d2, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [e3], c3, d3, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %4, %5, t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [e1], f1, g1, %5, t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [e2], f2, g2, %5, t;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [e3], f3, g3, %5, t;\n\t"
+        "@e mbarrier.arrive.shared::cta.b64 _, [%7], n1;\n\t"
+        "@e mbarrier.arrive.shared::cta.b64 _, [%10];\n\t"
+        "@e mbarrier.arrive.shared::cta.b64 _, [%8], %9;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%8];\n\t}"
+        :: "r"(d_tmem), "l"(a0), "l"(b0), "l"(a1), "l"(b1), "r"(idesc), "r"(accumulate),
+           "r"(smem_u32(slot0)), "r"(smem_u32(slot1)), "r"(arrivals), "r"(smem_u32(x))
+        : "memory");
+  } else {
+    umma_chunk4(d_tmem, a0, b0, idesc, accumulate, slot0, arrivals, x);
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.shared::cta.b64 _, [%0], %1;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+        :: "r"(smem_u32(slot1)), "r"(arrivals) : "memory");
+  }
+}
+
 // arrive on an mbarrier once all previously issued tcgen05.mma of this thread complete
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"

@@ -100,10 +100,14 @@ def run(N, K, B, ksplit, debug=0, steps=5, check=False):
 if __name__ == "__main__":
     out = []
     shapes = [(24576, 4096), (8192, 12288), (98304, 4096)]
+    if os.environ.get("SHAPES"):      # e.g. SHAPES=98304x4096,24576x4096
+        shapes = [tuple(int(v) for v in sh.split("x")) for sh in os.environ["SHAPES"].split(",")]
+    batches = [int(v) for v in os.environ.get("BATCHES", "16,64").split(",")]
+    kss = [bool(int(v)) for v in os.environ.get("KSPLIT", "0,1").split(",")]
     dbgs = [int(v) for v in os.environ.get("DBG", "0,2,4").split(",")]
     for (N, K) in shapes:
-        for B in (16, 64):
-            for ks in (False, True):
+        for B in batches:
+            for ks in kss:
                 for dbg in dbgs:
                     gbs, ms, err, ctr = run(N, K, B, ks, dbg, check=True)
                     rec = dict(N=N, K=K, B=B, ksplit=ks, debug=dbg, gbs=round(gbs, 1),
