@@ -1932,6 +1932,9 @@ __device__ float block_sum(Smem& s, float v, int ct) {
 
 __device__ void run_rmsnorm(const KArgs& a, Smem& s, const mk_task& t, int ib, int ie, int ct) {
   const mk_norm_params& p = *P<mk_norm_params>(a, t);
+  // folded / fused into the consuming GEMM and no gather or statistics to
+  // produce: nothing to compute (the unit still orders and signals its event)
+  if (p.fused && !p.embed && !p.ss_out && !p.x_store) return;
   const uint16_t* gam = reinterpret_cast<const uint16_t*>(p.gamma);
   constexpr int kRegChunks = 16;     // rows up to 16 * 256 wide stay in registers
   if (p.d <= kRegChunks * 256) {
