@@ -162,6 +162,8 @@ def gemv_tiles(model: ModelConfig, machine: MachineConfig, graph_mode: str,
     rows = min(batch, t_m)
     r_plain = 16 if rows <= 4 else 32
     r_fused = 16 if rows <= 4 else 32
+    if os.environ.get("MK_GEMV_ROWS"):     # A/B knob: weight rows per ring slot
+        r_plain = r_fused = int(os.environ["MK_GEMV_ROWS"])
     out = {}
     for op in LINEAR_OPS:
         k, n = shard_gemm_dims(op, model, tp)

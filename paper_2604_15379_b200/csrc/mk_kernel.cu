@@ -107,6 +107,8 @@ struct KArgs {
   const uint8_t* params;
   uint32_t* ev_ctr;
   const int32_t* ev_req;
+  const int32_t* ev_dmask; // per event: bit g = signalled by one die task of group g (and
+                           // by nothing else): waiters poll those die counters directly
   uint32_t* die_ctr;       // [n_events][n_sched]
   uint32_t* sub_ctr;
   uint64_t* mailbox;       // [n_sched*W][kMailbox]
@@ -244,6 +246,24 @@ __device__ __forceinline__ bool pos_ok(const KArgs& a, int pos, int t_max, int r
   if (pos >= 0 && pos < t_max) return true;
   raise_error(a, MK_ERR_CONFIG, -100 - row);
   return false;
+}
+
+// Has event e fired in this launch?  req = ev_req[e], dmask = ev_dmask[e]
+// (both cached in the task descriptor by the mailbox warp).  ACQ: acquire
+// loads; otherwise relaxed (the caller fences once).
+template <bool ACQ>
+__device__ __forceinline__ bool ev_done(const KArgs& a, int e, int32_t req, int32_t dmask) {
+  if (dmask > 0) {
+    const uint32_t target = uint32_t(a.W) * a.epoch;
+    for (int g = 0; g < a.n_sched; ++g) {
+      if (!((dmask >> g) & 1)) continue;
+      const uint32_t* c = &a.die_ctr[size_t(e) * a.n_sched + g];
+      if ((int32_t)((ACQ ? ld_acquire(c) : ld_relaxed(c)) - target) < 0) return false;
+    }
+    return true;
+  }
+  const uint32_t target = uint32_t(req) * a.epoch;
+  return (int32_t)((ACQ ? ld_acquire(&a.ev_ctr[e]) : ld_relaxed(&a.ev_ctr[e])) - target) >= 0;
 }
 
 // Spin helper: returns false if the watchdog fired / the launch aborted.
@@ -1422,9 +1442,8 @@ __device__ void xload_warp(const KArgs& a, Smem& s) {
         for (int k = 0; k < 2 && ok; ++k) {
           const int e = k ? t.wait1 : t.wait0;
           if (e < 0) continue;
-          const uint32_t target = uint32_t(t.pad[k]) * a.epoch;
           Spin sp;
-          while ((int32_t)(ld_relaxed(&a.ev_ctr[e]) - target) < 0)
+          while (!ev_done<false>(a, e, t.pad[k], t.pad[2 + k]))
             if (!sp.ok(a, -15)) { ok = false; break; }
         }
         fence_acq_rel_gpu();
@@ -3130,6 +3149,8 @@ __device__ void mailbox_warp(const KArgs& a, Smem& s, int g, int worker) {
       mk_task& t = s.tcache[qi];
       t.pad[0] = t.wait0 >= 0 ? a.ev_req[t.wait0] : 0;
       t.pad[1] = t.wait1 >= 0 ? a.ev_req[t.wait1] : 0;
+      t.pad[2] = t.wait0 >= 0 ? a.ev_dmask[t.wait0] : 0;
+      t.pad[3] = t.wait1 >= 0 ? a.ev_dmask[t.wait1] : 0;
       s.tq[qi] = make_int4(u.task, u.item_begin, u.item_end, 0);
       mbar_arrive(&s.tq_full[qi]);
     }
@@ -3278,11 +3299,10 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
         for (int k = 0; k < 2; ++k) {
           const int e = waits[k];
           if (e < 0) continue;
-          const uint32_t target = uint32_t(t.pad[k]) * a.epoch;   // cached ev_req[e]
           Spin sp;
           for (;;) {
             ++polls;
-            if ((int32_t)(ld_acquire(&a.ev_ctr[e]) - target) >= 0) break;
+            if (ev_done<true>(a, e, t.pad[k], t.pad[2 + k])) break;
             if (!sp.ok(a, e)) break;
           }
         }
@@ -3331,6 +3351,7 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
     bar_sync(1, kCons);
     if (ct == 0) {
       if (a.trace) s.tr[5] = globaltimer();
+      const uint64_t t_done = a.log ? globaltimer() : 0;   // work done (before publishing)
       ++n_exec;
       if (t.signal >= 0) {
         if (t.level == MK_LEVEL_CHIPLET) {
@@ -3354,7 +3375,7 @@ __device__ void consumers(const KArgs& a, Smem& s, uint8_t* ring, int g, int wor
           ++n_glob;
         }
       }
-      if (a.log) log_rec(a, 1, ent.x, ent.y, gw, g, t_start, globaltimer());
+      if (a.log) log_rec(a, 1, ent.x, ent.y, gw, g, t_start, t_done);
       if (a.trace && n_exec <= (unsigned long long)a.trace_cap) {
         uint64_t* rec = a.trace + (size_t(gw) * a.trace_cap + (n_exec - 1)) * 8;
         rec[0] = uint64_t(uint32_t(ent.x)) | (uint64_t(uint32_t(ent.y)) << 32);
@@ -3532,6 +3553,7 @@ static int fail(int code, const std::string& msg) {
   } while (0)
 
 struct mk_handle {
+  int use_dmask = 1;             // waiters of die-task events poll die counters (MK_EV_DMASK=0: off)
   int device = 0;
   int num_sms = 0;
   int sched_mode = 0;
@@ -3558,6 +3580,7 @@ struct mk_handle {
   uint8_t* d_params = nullptr;
   uint32_t* d_ev_ctr = nullptr;
   int32_t* d_ev_req = nullptr;
+  int32_t* d_ev_dmask = nullptr;
   uint32_t* d_die_ctr = nullptr;
   uint32_t* d_sub_ctr = nullptr;
   uint64_t* d_mailbox = nullptr;
@@ -3899,6 +3922,7 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
   if (topo->num_sms != prop.multiProcessorCount)
     return fail(MK_ERR_CONFIG, "topology was probed on a different device");
   mk_handle* h = new mk_handle();
+  if (const char* ev = getenv("MK_EV_DMASK")) h->use_dmask = atoi(ev) != 0;
   h->device = device;
   h->num_sms = prop.multiProcessorCount;
   h->sched_mode = g->sched_mode;
@@ -3940,6 +3964,7 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
   DA(h->d_params, g->param_bytes + kPBytes);   // the cache copy reads kPBytes per block
   DA(h->d_ev_ctr, g->n_events);
   DA(h->d_ev_req, g->n_events);
+  DA(h->d_ev_dmask, g->n_events);
   DA(h->d_die_ctr, size_t(g->n_events) * g->n_schedulers);
   DA(h->d_sub_ctr, g->n_sub_ctrs);
   DA(h->d_mailbox, size_t(g->n_schedulers) * h->W * kMailbox);
@@ -3962,6 +3987,28 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
   if (g->param_bytes)
     CK(cudaMemcpy(h->d_params, g->params, g->param_bytes, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(h->d_ev_req, g->event_required, sizeof(int32_t) * g->n_events, cudaMemcpyHostToDevice));
+  {
+    // An event whose signallers are exactly one die task per scheduler group
+    // completes when those groups' die counters reach W per launch: waiters
+    // poll the die counters (acquire via the acq_rel RMW chain of the W
+    // arrivals) instead of the event counter, which the last arrival still
+    // bumps after its fence (ref two-level completion, runtime.py:432-480)
+    // but no longer on the critical path.
+    std::vector<int32_t> dm(std::max(1, g->n_events), 0), bad(std::max(1, g->n_events), 0);
+    for (int i = 0; i < g->n_tasks; ++i) {
+      const mk_task& t = g->tasks[i];
+      if (t.signal < 0 || t.signal >= g->n_events) continue;
+      const int grp = g->n_schedulers == 1 ? 0 : t.die;
+      if (t.level != MK_LEVEL_CHIPLET || grp < 0 || grp >= g->n_schedulers || grp >= 31 ||
+          (dm[t.signal] >> grp) & 1)
+        bad[t.signal] = 1;
+      else
+        dm[t.signal] |= 1 << grp;
+    }
+    for (int e = 0; e < g->n_events; ++e)
+      if (bad[e] || __builtin_popcount(uint32_t(dm[e])) != g->event_required[e] || !h->use_dmask) dm[e] = 0;
+    CK(cudaMemcpy(h->d_ev_dmask, dm.data(), sizeof(int32_t) * g->n_events, cudaMemcpyHostToDevice));
+  }
   CK(cudaMemcpy(h->d_die_of_sm, die_of_sm.data(), MK_MAX_SMS, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(h->d_group_size, h->group_size.data(), sizeof(int32_t) * MK_MAX_DIES,
                 cudaMemcpyHostToDevice));
@@ -4025,6 +4072,7 @@ int mk_step(mk_handle* h, void* stream) {
   KArgs a;
   a.tasks = h->d_tasks; a.units = h->d_units; a.sched_begin = h->d_sched_begin;
   a.params = h->d_params; a.ev_ctr = h->d_ev_ctr; a.ev_req = h->d_ev_req;
+  a.ev_dmask = h->d_ev_dmask;
   a.die_ctr = h->d_die_ctr; a.sub_ctr = h->d_sub_ctr; a.mailbox = h->d_mailbox;
   a.mb_head = h->d_mb_head; a.mb_tail = h->d_mb_tail; a.die_of_sm = h->d_die_of_sm;
   a.role_ctr = h->d_role_ctr; a.group_size = h->d_group_size; a.stats = h->d_stats;
@@ -4270,7 +4318,7 @@ int mk_destroy(mk_handle* h) {
   if (!h) return MK_OK;
   cudaSetDevice(h->device);
   cudaFree(h->d_tasks); cudaFree(h->d_units); cudaFree(h->d_sched_begin); cudaFree(h->d_params);
-  cudaFree(h->d_ev_ctr); cudaFree(h->d_ev_req); cudaFree(h->d_die_ctr); cudaFree(h->d_sub_ctr);
+  cudaFree(h->d_ev_ctr); cudaFree(h->d_ev_req); cudaFree(h->d_ev_dmask); cudaFree(h->d_die_ctr); cudaFree(h->d_sub_ctr);
   cudaFree(h->d_mailbox); cudaFree(h->d_mb_head); cudaFree(h->d_mb_tail); cudaFree(h->d_die_of_sm);
   cudaFree(h->d_role_ctr); cudaFree(h->d_group_size); cudaFree(h->d_stats); cudaFree(h->d_err);
   cudaFree(h->d_log); cudaFree(h->d_log_cursor); cudaFree(h->d_tile_log); cudaFree(h->d_tile_cursor);
