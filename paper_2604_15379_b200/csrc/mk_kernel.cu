@@ -248,7 +248,8 @@ __device__ __forceinline__ bool pos_ok(const KArgs& a, int pos, int t_max, int r
   return false;
 }
 
-// Has event e fired in this launch?  req = ev_req[e], dmask = ev_dmask[e]
+// Has event e fired in this launch?  req = ev_req[e] (n_units in sub-counter
+// mode), dmask = ev_dmask[e]: > 0 die counters, < 0 the sub-counter -1-dmask
 // (both cached in the task descriptor by the mailbox warp).  ACQ: acquire
 // loads; otherwise relaxed (the caller fences once).
 template <bool ACQ>
@@ -263,7 +264,8 @@ __device__ __forceinline__ bool ev_done(const KArgs& a, int e, int32_t req, int3
     return true;
   }
   const uint32_t target = uint32_t(req) * a.epoch;
-  return (int32_t)((ACQ ? ld_acquire(&a.ev_ctr[e]) : ld_relaxed(&a.ev_ctr[e])) - target) >= 0;
+  const uint32_t* c = dmask < 0 ? &a.sub_ctr[-1 - dmask] : &a.ev_ctr[e];
+  return (int32_t)((ACQ ? ld_acquire(c) : ld_relaxed(c)) - target) >= 0;
 }
 
 // Spin helper: returns false if the watchdog fired / the launch aborted.
@@ -3994,10 +3996,17 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
     // arrivals) instead of the event counter, which the last arrival still
     // bumps after its fence (ref two-level completion, runtime.py:432-480)
     // but no longer on the critical path.
+    // Likewise an event signalled by one fanned-out CU task alone: waiters
+    // poll its unit sub-counter for n_units arrivals (dmask = -1 - sub_ctr,
+    // the cached requirement becomes n_units).
     std::vector<int32_t> dm(std::max(1, g->n_events), 0), bad(std::max(1, g->n_events), 0);
+    std::vector<int32_t> nsig(std::max(1, g->n_events), 0), last(std::max(1, g->n_events), -1);
+    std::vector<int32_t> req(g->event_required, g->event_required + g->n_events);
     for (int i = 0; i < g->n_tasks; ++i) {
       const mk_task& t = g->tasks[i];
       if (t.signal < 0 || t.signal >= g->n_events) continue;
+      ++nsig[t.signal];
+      last[t.signal] = i;
       const int grp = g->n_schedulers == 1 ? 0 : t.die;
       if (t.level != MK_LEVEL_CHIPLET || grp < 0 || grp >= g->n_schedulers || grp >= 31 ||
           (dm[t.signal] >> grp) & 1)
@@ -4005,9 +4014,19 @@ int mk_create(int device, const mk_graph_desc* g, const mk_topology* topo, mk_ha
       else
         dm[t.signal] |= 1 << grp;
     }
-    for (int e = 0; e < g->n_events; ++e)
+    for (int e = 0; e < g->n_events; ++e) {
       if (bad[e] || __builtin_popcount(uint32_t(dm[e])) != g->event_required[e] || !h->use_dmask) dm[e] = 0;
+      if (h->use_dmask && nsig[e] == 1 && g->event_required[e] == 1) {
+        const mk_task& t = g->tasks[last[e]];
+        if (t.level != MK_LEVEL_CHIPLET && t.n_units > 1 && t.sub_ctr >= 0 && t.sub_ctr < g->n_sub_ctrs) {
+          dm[e] = -1 - t.sub_ctr;
+          req[e] = t.n_units;
+        }
+      }
+    }
     CK(cudaMemcpy(h->d_ev_dmask, dm.data(), sizeof(int32_t) * g->n_events, cudaMemcpyHostToDevice));
+    // cached per waiter as the poll target multiplier (ev_req is read nowhere else)
+    CK(cudaMemcpy(h->d_ev_req, req.data(), sizeof(int32_t) * g->n_events, cudaMemcpyHostToDevice));
   }
   CK(cudaMemcpy(h->d_die_of_sm, die_of_sm.data(), MK_MAX_SMS, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(h->d_group_size, h->group_size.data(), sizeof(int32_t) * MK_MAX_DIES,
