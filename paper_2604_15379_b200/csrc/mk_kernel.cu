@@ -2826,10 +2826,15 @@ __device__ void run_attn_reduce(const KArgs& a, Smem& s, const mk_task& t, int i
   const int stride = G * (HD + 4);          // floats per split
   uint16_t* out = reinterpret_cast<uint16_t*>(p.out);
   constexpr int kBatch = 20;
-  for (int b = ib; b < ie; ++b) {
+  // the unit's rows x (G heads x HD/4 dim quads) flattened over all consumer
+  // threads: several rows merge in one round trip (G*HD/4 = 128 < kCons)
+  const int per_row = G * HD / 4;
+  const int n_work = (ie - ib) * per_row;
+  for (int idx = ct; idx < n_work; idx += kCons) {
+    const int b = ib + idx / per_row, e = idx % per_row;   // 4 dims per thread
     const int nv = min(row_pos(p.positions, b) / p.split + 1, p.n_splits);
     const float* base = p.partial + (size_t(b) * p.kv_heads + p.kv_head) * p.n_splits * stride;
-    for (int e = ct; e < G * HD / 4; e += kCons) {   // 4 dims per thread
+    {
       const int hh = (e * 4) / HD, d = (e * 4) % HD;
       const float* hb = base + hh * (HD + 4);
       float M = -INFINITY, den = 0.f;
