@@ -1702,6 +1702,12 @@ __device__ __forceinline__ void umma_epi16(const KArgs& a, Smem& s, const mk_gem
 // registers -> epilogue.  A K-split piece goes to the
 // worker's piece slot ([col][128 rows] fp32, coalesced); the last piece of a
 // tile sums all pieces in piece order and runs the epilogue.
+#ifndef MK_PIECES_IN_FLIGHT
+#define MK_PIECES_IN_FLIGHT 3
+#endif
+constexpr int kPiecesInFlight = MK_PIECES_IN_FLIGHT;   // K-split owner: piece loads per round trip
+                                                         // (4 / 6 measured slower: B=64 +1.5 / +2.3 %)
+
 __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, int w_in_task,
                               int ct, uint32_t& tb_k) {
   const int NT = umma_nt(p);
@@ -1803,10 +1809,10 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
       float rv[16], v[16];
       umma_res16(p, m0, rows_m, out_col0 + row, j, rv);
       tmem_acc16(s.tmem_base, q, buf, j, v);
-      for (int w0 = pi.first_w + 1; w0 <= pi.last_w; w0 += 3) {
-        float t[3][16];
+      for (int w0 = pi.first_w + 1; w0 <= pi.last_w; w0 += kPiecesInFlight) {
+        float t[kPiecesInFlight][16];
 #pragma unroll
-        for (int u = 0; u < 3; ++u) {
+        for (int u = 0; u < kPiecesInFlight; ++u) {
           const int w = w0 + u;
           const bool on = w <= pi.last_w && !pi.empty(w);
           const float* src = piece_ptr(p, on ? w : pi.first_w, 0);
@@ -1815,7 +1821,7 @@ __device__ void umma_epilogue(const KArgs& a, Smem& s, const mk_gemm_params& p, 
             t[u][i] = (on && 16 * j + i < rows_m) ? __ldcg(src + (16 * j + i) * 128 + row) : 0.f;
         }
 #pragma unroll
-        for (int u = 0; u < 3; ++u)
+        for (int u = 0; u < kPiecesInFlight; ++u)
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] += t[u][i];
       }
